@@ -1,0 +1,58 @@
+"""B200-native pipelined Krylov solvers (CG, BiCGStab, GMRES(m); CSR, fp64).
+
+A drop-in for the pipelined solve path of the reference package
+``pipekrylov`` (arXiv 1410.4054): the same driver names and signatures, the
+same result/config/context/trace types, bit-identical results at the same
+reduction geometry -- computed by hand-written sm_100a kernels in
+libpk_b200.so (C ABI in include/pipekrylov_b200.h), with no CPU fallback.
+"""
+
+from .device import DeviceContext, DeviceMatrix, context_for, device_matrix
+from .generators import (
+    convdiff2d,
+    convdiff3d,
+    gen_poisson2d,
+    gen_poisson3d_block,
+    poisson2d_grid,
+    poisson3d_grid,
+)
+from .linalg import (
+    DEFAULT_CONTEXT,
+    CsrMatrix,
+    ExecutionContext,
+    ExecutionTrace,
+    PhaseRecord,
+    WorkgroupPartials,
+    as_vector,
+)
+from .solvers import (
+    BREAKDOWN,
+    CLASSICAL_GS,
+    CONVERGED,
+    DEFAULT_BREAKDOWN_TOLERANCE,
+    LUCKY_BREAKDOWN,
+    MAX_ITER,
+    MODIFIED_GS,
+    SOLVERS,
+    BreakdownError,
+    SolverConfig,
+    SolverResult,
+    UpperTriangular,
+    bicgstab_pipelined,
+    cg_pipelined,
+    gmres_pipelined,
+    solve,
+    solve_upper_triangular,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BREAKDOWN", "CLASSICAL_GS", "CONVERGED", "DEFAULT_BREAKDOWN_TOLERANCE", "DEFAULT_CONTEXT",
+    "LUCKY_BREAKDOWN", "MAX_ITER", "MODIFIED_GS", "SOLVERS", "BreakdownError", "CsrMatrix",
+    "DeviceContext", "DeviceMatrix", "ExecutionContext", "ExecutionTrace", "PhaseRecord", "SolverConfig",
+    "SolverResult", "UpperTriangular", "WorkgroupPartials", "as_vector", "bicgstab_pipelined",
+    "cg_pipelined", "context_for", "convdiff2d", "convdiff3d", "device_matrix", "gen_poisson2d",
+    "gen_poisson3d_block", "gmres_pipelined", "poisson2d_grid", "poisson3d_grid", "solve",
+    "solve_upper_triangular", "__version__",
+]

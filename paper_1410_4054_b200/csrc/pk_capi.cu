@@ -1,0 +1,865 @@
+// C ABI of the B200-native pipelined Krylov path: contexts, matrices,
+// kernel-level entries (fused.py / linalg.py mirrors) and the solver-level
+// drivers (solvers.py pipelined variants) with device-resident loops.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo
+//        -fmad=false -Xcompiler -fPIC,-ffp-contract=off -shared
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pipekrylov_b200.h"
+#include "pk_kernels.cuh"
+#include "pk_reduce.cuh"
+#include "pk_state.cuh"
+
+using namespace pk;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define PK_CUDA(call)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? PK_ERR_NOMEM : PK_ERR_CUDA,            \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                     \
+    }                                                                                      \
+  } while (0)
+
+#define PK_TRY(...)              \
+  do {                           \
+    int rc_ = (__VA_ARGS__);     \
+    if (rc_ != PK_OK) return rc_; \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// objects
+// ---------------------------------------------------------------------------
+
+struct pk_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int32_t ng = 128;
+  int32_t gs = 256;
+  int sm_count = 148;
+  SolveState* scratch = nullptr;  // kernel-level finalizer state
+  int32_t* scratch_flag = nullptr;
+  double* scratch_d = nullptr;
+};
+
+struct pk_mat {
+  int device = 0;
+  int64_t n_rows = 0, n_cols = 0, nnz = 0, max_row = 0;
+  bool row64 = false;
+  void* rowptr = nullptr;
+  int32_t* cols = nullptr;
+  double* vals = nullptr;
+};
+
+static int set_device(int dev) {
+  PK_CUDA(cudaSetDevice(dev));
+  return PK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+
+template <int NQ, int U, class Op>
+__global__ void __launch_bounds__(256) k_reduce(Geom geo, Op op, ScalarPtrs sp, double* part, int ld,
+                                                int col0, SolveState* st, int gate,
+                                                const int32_t* skip, int fin, int fin_arg) {
+  extern __shared__ double smem[];
+  if (skip && *(volatile const int32_t*)skip) return;
+  if (st && !gate_open(st, gate)) return;
+  op.scalars(sp);
+  stage1_all_groups<NQ, U>(geo, op, smem, part, ld, col0);
+  if (fin != FIN_NONE && st) {
+    if (elect_last_block(&st->ticket)) finalize(st, fin, fin_arg);
+  }
+}
+
+template <int U, class Op>
+__global__ void __launch_bounds__(256) k_sweep(int64_t n, Op op, SolveState* st, int gate) {
+  if (st && !gate_open(st, gate)) return;
+  sweep_all<U>(n, op);
+}
+
+__global__ void k_finalize(SolveState* st, int fin, int arg) { finalize(st, fin, arg); }
+
+// totals[q] = serial sum of column q (reduce_stage2 / in-kernel finalize)
+__global__ void k_stage2(const double* part, int ng, int ld, int nq, double* out) {
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) out[q] = stage2_col(part, ng, ld, q);
+}
+
+__global__ void k_bicg_alpha(const double* rr0p, const double* aprp, int ng, double btol,
+                             double* alpha_out, int32_t* bd) {
+  __shared__ double t[2];
+  if (threadIdx.x == 0) t[0] = stage2_col(rr0p, ng, 1, 0);
+  if (threadIdx.x == 1) t[1] = stage2_col(aprp, ng, 1, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (fabs(t[1]) < btol) {
+      *bd = 1;
+    } else {
+      *bd = 0;
+      *alpha_out = div_rn(t[0], t[1]);
+    }
+  }
+}
+
+__global__ void k_norm_fin(const double* part, int ng, double btol, double* norm_out, double* inv_out,
+                           int32_t* lucky) {
+  if (threadIdx.x == 0) {
+    double nrm = __dsqrt_rn(stage2_col(part, ng, 1, 0));
+    *norm_out = nrm;
+    if (nrm < btol || nrm == 0.0) {
+      *lucky = 1;
+    } else {
+      *lucky = 0;
+      *inv_out = div_rn(1.0, nrm);
+    }
+  }
+}
+
+// y = y + alpha x with alpha from device memory (axpy, linalg.py:403-411)
+__global__ void k_axpy_dev(int64_t n, double* y, const double* x, const double* alpha) {
+  double a = *alpha;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = add_rn(y[i], mul_rn(a, x[i]));
+}
+
+// y = y * s (scale, linalg.py:440-447), s host value
+__global__ void k_scale(int64_t n, double* y, double s) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = mul_rn(y[i], s);
+}
+
+// GMRES iterate update (solvers.py:981-984):
+//   u = eta0 r; u = u + eta_k V_{k-1} (k = 1..ks-1); x = x + rho u
+__global__ void k_gmres_x(int64_t n, double* x, const double* r, const double* V, int64_t ldv,
+                          const double* eta, int ks, double rho) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double u = mul_rn(eta[0], r[i]);
+    for (int k = 1; k < ks; ++k) u = add_rn(u, mul_rn(eta[k], V[(int64_t)(k - 1) * ldv + i]));
+    x[i] = add_rn(x[i], mul_rn(rho, u));
+  }
+}
+
+__global__ void k_fill_i32(int32_t* p, int32_t v) { *p = v; }
+
+// ---------------------------------------------------------------------------
+// device-side generators
+// ---------------------------------------------------------------------------
+
+struct StencilSpec {
+  int32_t nent;
+  int64_t off[8];     // column offset, sorted ascending
+  int32_t axis[8];    // -1 for the diagonal
+  int32_t step[8];
+  double val[8];
+  int64_t dim[3];
+  int64_t stride[3];
+};
+
+__device__ __forceinline__ bool stencil_valid(const StencilSpec& s, int64_t row, int e) {
+  int ax = s.axis[e];
+  if (ax < 0) return true;
+  int64_t c = (row / s.stride[ax]) % s.dim[ax];
+  int64_t t = c + s.step[e];
+  return t >= 0 && t < s.dim[ax];
+}
+
+__global__ void k_gen_count(int64_t n, StencilSpec s, int64_t* counts) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int e = 0; e < s.nent; ++e) c += stencil_valid(s, i, e);
+    counts[i] = c;
+  }
+}
+
+template <typename RowT>
+__global__ void k_gen_fill(int64_t n, StencilSpec s, const RowT* rowptr, int32_t* cols, double* vals) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    RowT k = rowptr[i];
+    for (int e = 0; e < s.nent; ++e) {
+      if (stencil_valid(s, i, e)) {
+        cols[k] = (int32_t)(i + s.off[e]);
+        vals[k] = s.val[e];
+        ++k;
+      }
+    }
+  }
+}
+
+// exclusive scan of row counts (single pass per block + block sums); simple
+// three-kernel decoupled scan, run once per generated matrix.
+__global__ void k_scan_block(const int64_t* in, int64_t* out, int64_t n, int64_t* block_sums) {
+  __shared__ int64_t s[1024];
+  int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  int64_t v = i < n ? in[i] : 0;
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    int64_t t = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+    __syncthreads();
+    s[threadIdx.x] += t;
+    __syncthreads();
+  }
+  if (i < n) out[i] = s[threadIdx.x];  // inclusive
+  if (threadIdx.x == 1023) block_sums[blockIdx.x] = s[1023];
+}
+
+__global__ void k_scan_add(int64_t* out, int64_t n, const int64_t* block_prefix) {
+  int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  if (i < n && blockIdx.x > 0) out[i] += block_prefix[blockIdx.x - 1];
+}
+
+template <typename RowT>
+__global__ void k_rowptr_from_incl(const int64_t* incl, int64_t n, RowT* rowptr) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    rowptr[i] = (RowT)(i == 0 ? 0 : incl[i - 1]);
+}
+
+__global__ void k_rowptr_widen(const int32_t* rp32, int64_t n, int64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = rp32[i];
+}
+
+__global__ void k_row_max(const int64_t* counts, int64_t n, unsigned long long* mx) {
+  unsigned long long m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)counts[i]);
+  atomicMax(mx, m);
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+
+static int grid_for(const pk_ctx* c, int64_t groups) {
+  int64_t cap = (int64_t)c->sm_count * 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(groups, cap));
+}
+
+static int grid_elem(const pk_ctx* c, int64_t n, int block) {
+  int64_t want = (n + block - 1) / block;
+  int64_t cap = (int64_t)c->sm_count * 16;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
+}
+
+template <int NQ, int U, class Op>
+static int launch_reduce(const pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp,
+                         double* part, int ld, int col0, SolveState* st = nullptr, int gate = GATE_NONE,
+                         const int32_t* skip = nullptr, int fin = FIN_NONE, int fin_arg = 0) {
+  Geom geo = make_geom(n, c->ng, c->gs, 256);
+  size_t smem = engine_smem_bytes(geo, NQ);
+  auto kern = k_reduce<NQ, U, Op>;
+  if (smem > 48 * 1024) {
+    if (smem > 227 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
+    PK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  kern<<<grid_for(c, c->ng), geo.T, smem, s>>>(geo, op, sp, part, ld, col0, st, gate, skip, fin, fin_arg);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}
+
+template <int U, class Op>
+static int launch_sweep(const pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, SolveState* st = nullptr,
+                        int gate = GATE_NONE) {
+  k_sweep<U, Op><<<grid_elem(c, n, 256), 256, 0, s>>>(n, op, st, gate);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}
+
+template <typename RowT>
+static Csr<RowT> csr_of(const pk_mat* a) {
+  return Csr<RowT>{(const RowT*)a->rowptr, a->cols, a->vals};
+}
+
+// SpMV with NQ fused dots; dispatch on row index type and register width.
+template <int NQ, typename RowT, int W>
+static int spmv_fused_t(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q,
+                        const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
+                        SolveState* st, int gate, int fin, int fin_arg) {
+  OpSpmvFused<RowT, W, NQ> op{};
+  op.A = csr_of<RowT>(a);
+  op.p = p;
+  op.q = q;
+  for (int k = 0; k < 4; ++k) { op.kind[k] = PK_DOT_RESULT; op.w[k] = nullptr; }
+  for (int k = 0; k < NQ; ++k) { op.kind[k] = kinds[k]; op.w[k] = w ? w[k] : nullptr; }
+  constexpr int U = W <= 4 ? 4 : 2;
+  if constexpr (NQ == 0) {
+    return launch_sweep<U>(c, s, a->n_rows, op, st, gate);
+  } else {
+    return launch_reduce<NQ, U>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
+  }
+}
+
+template <int NQ>
+static int spmv_fused_dispatch(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q,
+                               const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
+                               SolveState* st = nullptr, int gate = GATE_NONE, int fin = FIN_NONE,
+                               int fin_arg = 0) {
+  if (a->row64) {
+    if (a->max_row <= 4) return spmv_fused_t<NQ, int64_t, 4>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+    return spmv_fused_t<NQ, int64_t, 8>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+  }
+  if (a->max_row <= 4) return spmv_fused_t<NQ, int32_t, 4>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+  return spmv_fused_t<NQ, int32_t, 8>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+}
+
+static int spmv_fused_any(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q, int nq,
+                          const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
+                          SolveState* st = nullptr, int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0) {
+  switch (nq) {
+    case 0: return spmv_fused_dispatch<0>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+    case 1: return spmv_fused_dispatch<1>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+    case 2: return spmv_fused_dispatch<2>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+    case 3: return spmv_fused_dispatch<3>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+    case 4: return spmv_fused_dispatch<4>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+    default: return fail(PK_ERR_INVALID, "spmv_fused carries 1 to 4 quantities");
+  }
+}
+
+template <typename RowT, int W>
+static int residual_t(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* x, const double* b,
+                      double* r, double* copy1, double* copy2, double* part, SolveState* st, int gate, int fin,
+                      int fin_arg) {
+  OpResidual<RowT, W> op{csr_of<RowT>(a), x, b, r, copy1, copy2};
+  constexpr int U = W <= 4 ? 4 : 2;
+  return launch_reduce<1, U>(c, s, a->n_rows, op, ScalarPtrs{}, part, 1, 0, st, gate, nullptr, fin, fin_arg);
+}
+
+// r = b - A x (+ copies) with <r,r> partials.
+static int residual_any(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* x, const double* b,
+                        double* r, double* copy1, double* copy2, double* part, SolveState* st = nullptr,
+                        int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0) {
+  if (a->row64) {
+    if (a->max_row <= 4) return residual_t<int64_t, 4>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg);
+    return residual_t<int64_t, 8>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg);
+  }
+  if (a->max_row <= 4) return residual_t<int32_t, 4>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg);
+  return residual_t<int32_t, 8>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg);
+}
+
+static int dot_partials(const pk_ctx* c, cudaStream_t s, int64_t n, const double* x, const double* y,
+                        double* part, SolveState* st = nullptr, int gate = GATE_NONE, int fin = FIN_NONE,
+                        int fin_arg = 0) {
+  OpDot op{x, y};
+  return launch_reduce<1, 8>(c, s, n, op, ScalarPtrs{}, part, 1, 0, st, gate, nullptr, fin, fin_arg);
+}
+
+template <int NB>
+static int multidot_t(const pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* const* basis,
+                      const double* v, double* part, int ld, int col0, SolveState* st, int gate, int fin,
+                      int fin_arg) {
+  OpMultiDot<NB> op{};
+  op.v = v;
+  op.nb = nb;
+  for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
+  constexpr int U = NB <= 2 ? 4 : (NB <= 8 ? 2 : 1);
+  return launch_reduce<NB, U>(c, s, n, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
+}
+
+// Largest NB whose leaf stack fits in shared memory for this geometry.
+static int multidot_nb_cap(const pk_ctx* c, int64_t n) {
+  Geom geo = make_geom(n, c->ng, c->gs, 256);
+  for (int nb : {32, 16, 8, 4, 2, 1}) {
+    if (engine_smem_bytes(geo, nb) <= 200 * 1024) return nb;
+  }
+  return 1;
+}
+
+// <b_j, v> partials for nb vectors, in passes of at most the smem cap.
+static int multidot_any(const pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* const* basis,
+                        const double* v, double* part, int ld, int col0, SolveState* st = nullptr,
+                        int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0) {
+  int cap = multidot_nb_cap(c, n);
+  int done = 0;
+  while (done < nb) {
+    int todo = std::min(nb - done, cap);
+    bool last = done + todo == nb;
+    int f = last ? fin : FIN_NONE;
+    int rc;
+    if (todo <= 1) rc = multidot_t<1>(c, s, n, todo, basis + done, v, part, ld, col0 + done, st, gate, f, fin_arg);
+    else if (todo <= 2) rc = multidot_t<2>(c, s, n, todo, basis + done, v, part, ld, col0 + done, st, gate, f, fin_arg);
+    else if (todo <= 4) rc = multidot_t<4>(c, s, n, todo, basis + done, v, part, ld, col0 + done, st, gate, f, fin_arg);
+    else if (todo <= 8) rc = multidot_t<8>(c, s, n, todo, basis + done, v, part, ld, col0 + done, st, gate, f, fin_arg);
+    else if (todo <= 16) rc = multidot_t<16>(c, s, n, todo, basis + done, v, part, ld, col0 + done, st, gate, f, fin_arg);
+    else rc = multidot_t<32>(c, s, n, todo, basis + done, v, part, ld, col0 + done, st, gate, f, fin_arg);
+    PK_TRY(rc);
+    done += todo;
+  }
+  return PK_OK;
+}
+
+template <int NB>
+static int gs_update_t(const pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
+                       const double* coef_dev, double* part, SolveState* st, int gate, int fin, int fin_arg) {
+  OpGsUpdate<NB> op{};
+  op.v = v;
+  op.nb = nb;
+  for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
+  ScalarPtrs sp{coef_dev, nullptr, nullptr};
+  constexpr int U = NB <= 2 ? 4 : (NB <= 8 ? 2 : 1);
+  return launch_reduce<1, U>(c, s, n, op, sp, part, 1, 0, st, gate, nullptr, fin, fin_arg);
+}
+
+static int gs_update_any(const pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
+                         const double* coef_dev, double* part, SolveState* st = nullptr, int gate = GATE_NONE,
+                         int fin = FIN_NONE, int fin_arg = 0) {
+  if (nb <= 1) return gs_update_t<1>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
+  if (nb <= 2) return gs_update_t<2>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
+  if (nb <= 4) return gs_update_t<4>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
+  if (nb <= 8) return gs_update_t<8>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
+  if (nb <= 16) return gs_update_t<16>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
+  if (nb <= 32) return gs_update_t<32>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
+  return fail(PK_ERR_UNSUPPORTED, "Gram-Schmidt update supports at most 32 basis vectors (restart <= 33)");
+}
+
+// ---------------------------------------------------------------------------
+// library / contexts
+// ---------------------------------------------------------------------------
+
+extern "C" const char* pk_last_error(void) { return g_err.c_str(); }
+extern "C" int pk_abi_version(void) { return PK_ABI_VERSION; }
+
+extern "C" int pk_device_count(int* count) {
+  if (!count) return fail(PK_ERR_INVALID, "count is NULL");
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(PK_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  return PK_OK;
+}
+
+extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, pk_ctx** out) {
+  if (!out) return fail(PK_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (n_groups < 1) return fail(PK_ERR_INVALID, "n_groups must be >= 1, got " + std::to_string(n_groups));
+  if (group_size < 1 || (group_size & (group_size - 1)) != 0)
+    return fail(PK_ERR_INVALID, "group_size must be a positive power of two, got " + std::to_string(group_size));
+  if (n_groups > (1ll << 30) || group_size > (1ll << 30))
+    return fail(PK_ERR_UNSUPPORTED, "geometry too large for the device path");
+  PK_TRY(set_device(device));
+  pk_ctx* c = new pk_ctx();
+  c->device = device;
+  c->ng = (int32_t)n_groups;
+  c->gs = (int32_t)group_size;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&c->scratch, sizeof(SolveState));
+  if (e == cudaSuccess) e = cudaMalloc(&c->scratch_flag, 64 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->scratch_d, 64 * sizeof(double));
+  if (e != cudaSuccess) {
+    pk_ctx_destroy(c);
+    return fail(PK_ERR_CUDA, std::string("context allocation: ") + cudaGetErrorString(e));
+  }
+  c->stream = c->own;
+  // keep freed workspace memory in the stream-ordered pool between solves
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return PK_OK;
+}
+
+extern "C" int pk_ctx_destroy(pk_ctx* c) {
+  if (!c) return PK_OK;
+  cudaSetDevice(c->device);
+  if (c->own) cudaStreamSynchronize(c->own);
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->scratch_flag) cudaFree(c->scratch_flag);
+  if (c->scratch_d) cudaFree(c->scratch_d);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return PK_OK;
+}
+
+extern "C" int pk_ctx_set_stream(pk_ctx* c, void* stream) {
+  if (!c) return fail(PK_ERR_INVALID, "ctx is NULL");
+  c->stream = stream ? (cudaStream_t)stream : c->own;
+  return PK_OK;
+}
+
+extern "C" int pk_ctx_synchronize(pk_ctx* c) {
+  if (!c) return fail(PK_ERR_INVALID, "ctx is NULL");
+  PK_CUDA(cudaStreamSynchronize(c->stream));
+  return PK_OK;
+}
+
+extern "C" int pk_ctx_geometry(const pk_ctx* c, int64_t* ng, int64_t* gs) {
+  if (!c) return fail(PK_ERR_INVALID, "ctx is NULL");
+  if (ng) *ng = c->ng;
+  if (gs) *gs = c->gs;
+  return PK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// matrices
+// ---------------------------------------------------------------------------
+
+static int alloc_mat(pk_ctx* c, int64_t n_rows, int64_t n_cols, int64_t nnz, pk_mat** out) {
+  pk_mat* m = new pk_mat();
+  m->device = c->device;
+  m->n_rows = n_rows;
+  m->n_cols = n_cols;
+  m->nnz = nnz;
+  m->row64 = nnz >= (1ll << 31) - 1;
+  size_t rsz = (size_t)(n_rows + 1) * (m->row64 ? 8 : 4);
+  // pad arrays so vectorised/bulk loads may read a little past the end
+  cudaError_t e = cudaMalloc(&m->rowptr, rsz + 64);
+  if (e == cudaSuccess) e = cudaMalloc(&m->cols, (size_t)nnz * 4 + 64);
+  if (e == cudaSuccess) e = cudaMalloc(&m->vals, (size_t)nnz * 8 + 64);
+  if (e != cudaSuccess) {
+    pk_mat_destroy(m);
+    return fail(e == cudaErrorMemoryAllocation ? PK_ERR_NOMEM : PK_ERR_CUDA,
+                std::string("matrix allocation: ") + cudaGetErrorString(e));
+  }
+  *out = m;
+  return PK_OK;
+}
+
+extern "C" int pk_csr_upload(pk_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* offs, const int64_t* cols,
+                             const double* vals, pk_mat** out) {
+  if (!c || !out || !offs) return fail(PK_ERR_INVALID, "NULL argument");
+  *out = nullptr;
+  // canonical-form validation, linalg.py:86-111
+  if (n_rows < 0 || n_cols < 0) return fail(PK_ERR_INVALID, "matrix dimensions must be non-negative");
+  if (n_rows >= (1ll << 31) - 1 || n_cols >= (1ll << 31) - 1)
+    return fail(PK_ERR_UNSUPPORTED, "device path indexes rows and columns with int32");
+  if (offs[0] != 0) return fail(PK_ERR_INVALID, "row_offsets must start at 0");
+  int64_t max_row = 0;
+  for (int64_t i = 0; i < n_rows; ++i) {
+    int64_t d = offs[i + 1] - offs[i];
+    if (d < 0) return fail(PK_ERR_INVALID, "row_offsets must be non-decreasing");
+    max_row = std::max(max_row, d);
+  }
+  int64_t nnz = offs[n_rows];
+  if (nnz > 0 && (!cols || !vals)) return fail(PK_ERR_INVALID, "NULL column/value array");
+  for (int64_t i = 0; i < n_rows; ++i) {
+    for (int64_t k = offs[i]; k < offs[i + 1]; ++k) {
+      if (cols[k] < 0 || cols[k] >= n_cols) return fail(PK_ERR_INVALID, "column index out of range");
+      if (k > offs[i] && cols[k] <= cols[k - 1])
+        return fail(PK_ERR_INVALID, "column indices must be strictly increasing within each row");
+    }
+  }
+  PK_TRY(set_device(c->device));
+  pk_mat* m = nullptr;
+  PK_TRY(alloc_mat(c, n_rows, n_cols, nnz, &m));
+  m->max_row = max_row;
+  std::vector<int32_t> c32((size_t)nnz);
+  for (int64_t k = 0; k < nnz; ++k) c32[k] = (int32_t)cols[k];
+  cudaError_t e = cudaSuccess;
+  if (m->row64) {
+    e = cudaMemcpy(m->rowptr, offs, (size_t)(n_rows + 1) * 8, cudaMemcpyHostToDevice);
+  } else {
+    std::vector<int32_t> r32((size_t)n_rows + 1);
+    for (int64_t i = 0; i <= n_rows; ++i) r32[i] = (int32_t)offs[i];
+    e = cudaMemcpy(m->rowptr, r32.data(), r32.size() * 4, cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess && nnz) e = cudaMemcpy(m->cols, c32.data(), (size_t)nnz * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && nnz) e = cudaMemcpy(m->vals, vals, (size_t)nnz * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    pk_mat_destroy(m);
+    return fail(PK_ERR_CUDA, std::string("matrix upload: ") + cudaGetErrorString(e));
+  }
+  *out = m;
+  return PK_OK;
+}
+
+extern "C" int pk_csr_generate(pk_ctx* c, int32_t family, const int64_t* dims, int32_t ndims, const double* coef,
+                               int32_t ncoef, pk_mat** out) {
+  if (!c || !out || !dims) return fail(PK_ERR_INVALID, "NULL argument");
+  *out = nullptr;
+  StencilSpec sp{};
+  int nd = (family == PK_GEN_POISSON2D || family == PK_GEN_CONVDIFF2D) ? 2 : 3;
+  if (family < 0 || family > 3) return fail(PK_ERR_INVALID, "unknown generator family");
+  if (ndims != nd) return fail(PK_ERR_INVALID, "wrong number of grid dimensions");
+  int64_t n = 1;
+  for (int d = 0; d < nd; ++d) {
+    if (dims[d] < 1) return fail(PK_ERR_INVALID, "grid dimensions must be >= 1");
+    sp.dim[d] = dims[d];
+    sp.stride[d] = n;
+    n *= dims[d];
+  }
+  if (n >= (1ll << 31) - 1) return fail(PK_ERR_UNSUPPORTED, "grid too large for int32 row indices");
+  // per-direction values: {axis, step, value}
+  double diag = 0.0;
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  if (family == PK_GEN_POISSON2D || family == PK_GEN_POISSON3D) {
+    double dv = nd == 2 ? 4.0 : 12.0, ov = nd == 2 ? -1.0 : -2.0;
+    if (ncoef >= 2) { dv = coef[0]; ov = coef[1]; }
+    diag = dv;
+    for (int d = 0; d < nd; ++d) lo[d] = hi[d] = ov;
+  } else {
+    if (nd == 2 && dims[0] != dims[1]) return fail(PK_ERR_INVALID, "convection-diffusion grids are square");
+    if (nd == 3 && (dims[0] != dims[1] || dims[1] != dims[2]))
+      return fail(PK_ERR_INVALID, "convection-diffusion grids are cubic");
+    double cvel[3] = {1.0, 1.0, 1.0};
+    for (int d = 0; d < nd && d < ncoef; ++d) cvel[d] = coef[d];
+    volatile double h = 1.0 / (double)(dims[0] + 1);
+    // same expression trees as oracle.convdiff{2,3}d, no contraction
+    volatile double csum = nd == 2 ? cvel[0] + cvel[1] : (cvel[0] + cvel[1]) + cvel[2];
+    volatile double hc = h * csum;
+    diag = (nd == 2 ? 4.0 : 6.0) + hc;
+    for (int d = 0; d < nd; ++d) {
+      volatile double t = h * cvel[d];
+      lo[d] = -1.0 - t;
+      hi[d] = -1.0;
+    }
+  }
+  // entries sorted by column offset: -stride[nd-1] ... +stride[nd-1]
+  int e = 0;
+  for (int d = nd - 1; d >= 0; --d) { sp.off[e] = -sp.stride[d]; sp.axis[e] = d; sp.step[e] = -1; sp.val[e] = lo[d]; ++e; }
+  sp.off[e] = 0; sp.axis[e] = -1; sp.step[e] = 0; sp.val[e] = diag; ++e;
+  for (int d = 0; d < nd; ++d) { sp.off[e] = sp.stride[d]; sp.axis[e] = d; sp.step[e] = 1; sp.val[e] = hi[d]; ++e; }
+  sp.nent = e;
+
+  PK_TRY(set_device(c->device));
+  cudaStream_t s = c->stream;
+  int64_t* counts = nullptr;
+  int64_t* incl = nullptr;
+  int64_t nblk = (n + 1023) / 1024;
+  int64_t* bsum = nullptr;
+  int64_t* bsum_incl = nullptr;
+  unsigned long long* dmax = nullptr;
+  PK_CUDA(cudaMalloc(&counts, n * 8));
+  PK_CUDA(cudaMalloc(&incl, n * 8));
+  PK_CUDA(cudaMalloc(&bsum, nblk * 8));
+  PK_CUDA(cudaMalloc(&bsum_incl, nblk * 8));
+  PK_CUDA(cudaMalloc(&dmax, 8));
+  PK_CUDA(cudaMemsetAsync(dmax, 0, 8, s));
+  int g = grid_elem(c, n, 256);
+  k_gen_count<<<g, 256, 0, s>>>(n, sp, counts);
+  k_row_max<<<g, 256, 0, s>>>(counts, n, dmax);
+  k_scan_block<<<(unsigned)nblk, 1024, 0, s>>>(counts, incl, n, bsum);
+  // scan block sums on the host (nblk <= 2M)
+  std::vector<int64_t> hb((size_t)nblk);
+  PK_CUDA(cudaMemcpyAsync(hb.data(), bsum, nblk * 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long hmax = 0;
+  PK_CUDA(cudaMemcpyAsync(&hmax, dmax, 8, cudaMemcpyDeviceToHost, s));
+  PK_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 1; i < nblk; ++i) hb[i] += hb[i - 1];
+  int64_t nnz = nblk ? hb[nblk - 1] : 0;
+  PK_CUDA(cudaMemcpyAsync(bsum_incl, hb.data(), nblk * 8, cudaMemcpyHostToDevice, s));
+  k_scan_add<<<(unsigned)nblk, 1024, 0, s>>>(incl, n, bsum_incl);
+  pk_mat* m = nullptr;
+  int rc = alloc_mat(c, n, n, nnz, &m);
+  if (rc == PK_OK) {
+    m->max_row = (int64_t)hmax;
+    if (m->row64) {
+      k_rowptr_from_incl<int64_t><<<g, 256, 0, s>>>(incl, n, (int64_t*)m->rowptr);
+      k_gen_fill<int64_t><<<g, 256, 0, s>>>(n, sp, (const int64_t*)m->rowptr, m->cols, m->vals);
+    } else {
+      k_rowptr_from_incl<int32_t><<<g, 256, 0, s>>>(incl, n, (int32_t*)m->rowptr);
+      k_gen_fill<int32_t><<<g, 256, 0, s>>>(n, sp, (const int32_t*)m->rowptr, m->cols, m->vals);
+    }
+  }
+  cudaError_t ce = cudaStreamSynchronize(s);
+  cudaFree(counts);
+  cudaFree(incl);
+  cudaFree(bsum);
+  cudaFree(bsum_incl);
+  cudaFree(dmax);
+  if (rc != PK_OK) return rc;
+  if (ce != cudaSuccess) {
+    pk_mat_destroy(m);
+    return fail(PK_ERR_CUDA, std::string("generator: ") + cudaGetErrorString(ce));
+  }
+  *out = m;
+  return PK_OK;
+}
+
+extern "C" int pk_csr_info(const pk_mat* m, int64_t* n_rows, int64_t* n_cols, int64_t* nnz, int64_t* max_row) {
+  if (!m) return fail(PK_ERR_INVALID, "mat is NULL");
+  if (n_rows) *n_rows = m->n_rows;
+  if (n_cols) *n_cols = m->n_cols;
+  if (nnz) *nnz = m->nnz;
+  if (max_row) *max_row = m->max_row;
+  return PK_OK;
+}
+
+extern "C" int pk_csr_download(pk_ctx* c, const pk_mat* m, int64_t* offs, int64_t* cols, double* vals) {
+  if (!c || !m) return fail(PK_ERR_INVALID, "NULL argument");
+  PK_TRY(set_device(m->device));
+  if (offs) {
+    if (m->row64) {
+      PK_CUDA(cudaMemcpy(offs, m->rowptr, (size_t)(m->n_rows + 1) * 8, cudaMemcpyDeviceToHost));
+    } else {
+      std::vector<int32_t> r((size_t)m->n_rows + 1);
+      PK_CUDA(cudaMemcpy(r.data(), m->rowptr, r.size() * 4, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < r.size(); ++i) offs[i] = r[i];
+    }
+  }
+  if (cols && m->nnz) {
+    std::vector<int32_t> cc((size_t)m->nnz);
+    PK_CUDA(cudaMemcpy(cc.data(), m->cols, cc.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < cc.size(); ++i) cols[i] = cc[i];
+  }
+  if (vals && m->nnz) PK_CUDA(cudaMemcpy(vals, m->vals, (size_t)m->nnz * 8, cudaMemcpyDeviceToHost));
+  return PK_OK;
+}
+
+extern "C" int pk_mat_destroy(pk_mat* m) {
+  if (!m) return PK_OK;
+  cudaSetDevice(m->device);
+  if (m->rowptr) cudaFree(m->rowptr);
+  if (m->cols) cudaFree(m->cols);
+  if (m->vals) cudaFree(m->vals);
+  delete m;
+  return PK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel-level entries
+// ---------------------------------------------------------------------------
+
+#define PK_CHECK_CTX(c) \
+  do { if (!(c)) return fail(PK_ERR_INVALID, "ctx is NULL"); PK_TRY(set_device((c)->device)); } while (0)
+
+extern "C" int pk_spmv(pk_ctx* c, const pk_mat* a, const double* p, double* q) {
+  PK_CHECK_CTX(c);
+  if (!a || (!p && a->n_cols) || (!q && a->n_rows)) return fail(PK_ERR_INVALID, "NULL argument");
+  if (a->n_rows == 0) return PK_OK;
+  return spmv_fused_any(c, c->stream, a, p, q, 0, nullptr, nullptr, nullptr, 0, 0);
+}
+
+extern "C" int pk_spmv_fused(pk_ctx* c, const pk_mat* a, const double* p, double* q, int32_t nq,
+                             const int32_t* kinds, const double* const* w, double* partials) {
+  PK_CHECK_CTX(c);
+  if (!a || !kinds || !partials) return fail(PK_ERR_INVALID, "NULL argument");
+  if (nq < 1 || nq > 4) return fail(PK_ERR_INVALID, "request must carry 1 to 4 quantities, got " + std::to_string(nq));
+  for (int k = 0; k < nq; ++k) {
+    if (kinds[k] < 0 || kinds[k] > 2) return fail(PK_ERR_INVALID, "unknown quantity kind");
+    if (kinds[k] == PK_DOT_INPUT && a->n_rows != a->n_cols)
+      return fail(PK_ERR_INVALID, "result-with-input dot needs a square matrix");
+    if (kinds[k] == PK_DOT_VECTOR && (!w || !w[k])) return fail(PK_ERR_INVALID, "missing fixed dot vector");
+  }
+  return spmv_fused_any(c, c->stream, a, p, q, nq, kinds, w, partials, nq, 0);
+}
+
+extern "C" int pk_reduce_stage1(pk_ctx* c, int64_t n, int32_t nq, const double* const* columns, double* partials) {
+  PK_CHECK_CTX(c);
+  if (!columns || !partials || n < 0) return fail(PK_ERR_INVALID, "bad argument");
+  // one launch per block of up to 4 columns (stacking never reorders, test_linalg.py:198-207)
+  for (int q0 = 0; q0 < nq; q0 += 4) {
+    int k = std::min(4, nq - q0);
+    int rc;
+    switch (k) {
+      case 1: { OpColumns<1> op{{columns[q0]}}; rc = launch_reduce<1, 8>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      case 2: { OpColumns<2> op{{columns[q0], columns[q0 + 1]}}; rc = launch_reduce<2, 4>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      case 3: { OpColumns<3> op{{columns[q0], columns[q0 + 1], columns[q0 + 2]}}; rc = launch_reduce<3, 4>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      default: { OpColumns<4> op{{columns[q0], columns[q0 + 1], columns[q0 + 2], columns[q0 + 3]}}; rc = launch_reduce<4, 2>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+    }
+    PK_TRY(rc);
+  }
+  return PK_OK;
+}
+
+extern "C" int pk_reduce_stage2(pk_ctx* c, int32_t nq, const double* partials, double* totals) {
+  PK_CHECK_CTX(c);
+  if (!partials || !totals || nq < 0) return fail(PK_ERR_INVALID, "bad argument");
+  if (nq == 0) return PK_OK;
+  k_stage2<<<1, 32, 0, c->stream>>>(partials, c->ng, nq, nq, totals);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}
+
+extern "C" int pk_dot(pk_ctx* c, int64_t n, const double* x, const double* y, double* total) {
+  PK_CHECK_CTX(c);
+  if (!total || n < 0) return fail(PK_ERR_INVALID, "bad argument");
+  double* part = nullptr;
+  PK_CUDA(cudaMallocAsync(&part, (size_t)c->ng * 8, c->stream));
+  int rc = dot_partials(c, c->stream, n, x, y, part);
+  if (rc == PK_OK) {
+    k_stage2<<<1, 32, 0, c->stream>>>(part, c->ng, 1, 1, total);
+    if (cudaGetLastError() != cudaSuccess) rc = fail(PK_ERR_CUDA, "stage2 launch failed");
+  }
+  cudaFreeAsync(part, c->stream);
+  return rc;
+}
+
+extern "C" int pk_cg_update(pk_ctx* c, int64_t n, double* x, double* r, double* p, const double* ap, double alpha,
+                            double beta, double* partials) {
+  PK_CHECK_CTX(c);
+  if (!partials || n < 0) return fail(PK_ERR_INVALID, "bad argument");
+  OpCgUpdate op{x, r, p, ap, alpha, beta};
+  return launch_reduce<1, 8>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
+}
+
+extern "C" int pk_bicg_s_update(pk_ctx* c, int64_t n, const double* r, const double* ap, const double* rr0p,
+                                const double* aprp, double btol, double* s, double* partials, double* alpha_out,
+                                int32_t* breakdown) {
+  PK_CHECK_CTX(c);
+  if (!rr0p || !aprp || !partials || !alpha_out || !breakdown) return fail(PK_ERR_INVALID, "NULL argument");
+  k_bicg_alpha<<<1, 32, 0, c->stream>>>(rr0p, aprp, c->ng, btol, alpha_out, breakdown);
+  PK_CUDA(cudaGetLastError());
+  OpBicgS op{r, ap, s, 0.0};
+  ScalarPtrs sp{alpha_out, nullptr, nullptr};
+  return launch_reduce<1, 8>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, breakdown);
+}
+
+extern "C" int pk_bicg_xrp_update(pk_ctx* c, int64_t n, double* x, double* r, double* p, const double* s,
+                                  const double* ap, const double* as, double alpha, double omega, double beta,
+                                  const double* r0star, double* partials) {
+  PK_CHECK_CTX(c);
+  if (!partials || n < 0) return fail(PK_ERR_INVALID, "bad argument");
+  OpBicgXrp op{x, r, p, s, ap, as, r0star, alpha, omega, beta};
+  return launch_reduce<1, 4>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
+}
+
+extern "C" int pk_gs_stage1(pk_ctx* c, int64_t n, int32_t nb, const double* const* basis, const double* v,
+                            double* partials) {
+  PK_CHECK_CTX(c);
+  if (nb < 0 || (nb > 0 && (!basis || !partials))) return fail(PK_ERR_INVALID, "bad argument");
+  if (nb == 0) return PK_OK;
+  return multidot_any(c, c->stream, n, nb, basis, v, partials, nb, 0);
+}
+
+extern "C" int pk_gs_update(pk_ctx* c, int64_t n, double* v, int32_t nb, const double* const* basis,
+                            const double* partials, double* coeffs, double* norm_partials) {
+  PK_CHECK_CTX(c);
+  if (nb < 0 || !norm_partials || (nb > 0 && (!basis || !partials || !coeffs)))
+    return fail(PK_ERR_INVALID, "bad argument");
+  if (nb > 0) {
+    k_stage2<<<1, 32, 0, c->stream>>>(partials, c->ng, nb, nb, coeffs);
+    PK_CUDA(cudaGetLastError());
+  }
+  return gs_update_any(c, c->stream, n, v, nb, basis, coeffs, norm_partials);
+}
+
+extern "C" int pk_gs_normalize(pk_ctx* c, int64_t n, double* v, const double* norm_partials, const double* r,
+                               double btol, double* norm_out, int32_t* lucky, double* partials) {
+  PK_CHECK_CTX(c);
+  if (!norm_partials || !norm_out || !lucky || !partials) return fail(PK_ERR_INVALID, "NULL argument");
+  double* inv = c->scratch_d;
+  k_norm_fin<<<1, 32, 0, c->stream>>>(norm_partials, c->ng, btol, norm_out, inv, lucky);
+  PK_CUDA(cudaGetLastError());
+  OpNormalize op{v, r, 0.0};
+  ScalarPtrs sp{inv, nullptr, nullptr};
+  return launch_reduce<1, 8>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, lucky);
+}
+
+#include "pk_solvers.inc"

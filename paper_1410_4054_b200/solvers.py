@@ -1,0 +1,286 @@
+"""Pipelined Krylov drivers on B200 behind the reference's solver API.
+
+Drop-in for ``pipekrylov.SOLVERS[(method, "pipelined")]`` (reference
+__init__.py:81-88; solvers.py:395-469, 583-712, 865-1008): same signature
+``solver(a, b, x0=None, config=None, context=None, debug=False)``, same
+``SolverResult`` fields, same ``ValueError`` validation, and bit-identical
+numbers at the same ``ExecutionContext`` geometry.  The loop itself runs in
+libpk_b200.so: CG and BiCGStab as a conditional-WHILE CUDA graph with all
+scalar recurrences finalized on the device, GMRES(m) with one host round trip
+per restart cycle for the triangular solve (done here in NumPy, exactly as
+the reference does it).
+
+``solve(A, b, tag, tol, maxiter)`` is the north-star convenience entry.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .device import DeviceMatrix, context_for, device_matrix
+from .linalg import CHECK, FINISH, ITERATION, SETUP, CsrMatrix, ExecutionContext, ExecutionTrace, as_vector
+
+CONVERGED = "converged"
+MAX_ITER = "max_iter"
+BREAKDOWN = "breakdown"
+LUCKY_BREAKDOWN = "lucky_breakdown"
+CLASSICAL_GS = "classical_gs"
+MODIFIED_GS = "modified_gs"
+DEFAULT_BREAKDOWN_TOLERANCE = 1e-30
+
+
+class BreakdownError(RuntimeError):
+    """A recurrence divisor vanished (errors.py:6-18)."""
+
+    def __init__(self, kind: str, message: str = ""):
+        self.kind = kind
+        super().__init__(message or f"breakdown: {kind}")
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """Driver knobs (solvers.py:104-145) plus ``loop_mode``: "graph" (CUDA
+    graph with a device-side WHILE condition, default) or "host"."""
+
+    tolerance: float = 1e-8
+    max_iterations: int = 500
+    restart: int = 30
+    orthogonalization: str = CLASSICAL_GS
+    breakdown_tolerance: float = DEFAULT_BREAKDOWN_TOLERANCE
+    fixed_iterations: int | None = None
+    loop_mode: str = "graph"
+
+    def __post_init__(self):
+        if not (self.tolerance > 0):
+            raise ValueError("tolerance must be positive")
+        if self.max_iterations < 1:
+            raise ValueError("max_iterations must be at least 1")
+        if self.restart < 1:
+            raise ValueError("restart must be at least 1")
+        if self.orthogonalization not in (CLASSICAL_GS, MODIFIED_GS):
+            raise ValueError(f"unknown orthogonalization {self.orthogonalization!r}")
+        if not (self.breakdown_tolerance > 0):
+            raise ValueError("breakdown_tolerance must be positive")
+        if self.fixed_iterations is not None and self.fixed_iterations < 1:
+            raise ValueError("fixed_iterations must be at least 1 when set")
+        if self.loop_mode not in ("graph", "host"):
+            raise ValueError(f"unknown loop_mode {self.loop_mode!r}")
+
+    @property
+    def fixed(self) -> bool:
+        return self.fixed_iterations is not None
+
+    def iteration_limit(self) -> int:
+        return self.fixed_iterations if self.fixed else self.max_iterations
+
+    def loop_breakdown_tolerance(self) -> float:
+        return 0.0 if self.fixed else self.breakdown_tolerance
+
+    @classmethod
+    def coerce(cls, cfg) -> "SolverConfig":
+        if cfg is None:
+            return cls()
+        if isinstance(cfg, cls):
+            return cfg
+        # the reference's SolverConfig (same field names)
+        return cls(tolerance=cfg.tolerance, max_iterations=cfg.max_iterations, restart=cfg.restart,
+                   orthogonalization=cfg.orthogonalization, breakdown_tolerance=cfg.breakdown_tolerance,
+                   fixed_iterations=cfg.fixed_iterations)
+
+
+@dataclass
+class SolverResult:
+    """Outcome of one run (solvers.py:148-171)."""
+
+    x: np.ndarray
+    residual_history: list
+    true_final_residual: float
+    iterations: int
+    termination: str
+    trace: ExecutionTrace
+    breakdown_kind: str | None = None
+    loop_seconds: float = 0.0
+    diagnostics: dict = field(default_factory=dict)
+
+    @property
+    def converged(self) -> bool:
+        return self.termination == CONVERGED
+
+
+class UpperTriangular:
+    """Dense upper-triangular matrix filled column by column (solvers.py:174-202)."""
+
+    def __init__(self, order: int):
+        if order < 0:
+            raise ValueError("order must be non-negative")
+        self.order = order
+        self.data = np.zeros((order, order))
+
+    def set(self, row: int, col: int, value: float) -> None:
+        if not (0 <= row <= col < self.order):
+            raise ValueError(f"entry ({row}, {col}) is not in the upper triangle")
+        self.data[row, col] = value
+
+    def get(self, row: int, col: int) -> float:
+        if not (0 <= row <= col < self.order):
+            raise ValueError(f"entry ({row}, {col}) is not in the upper triangle")
+        return float(self.data[row, col])
+
+    def leading(self, k: int) -> "UpperTriangular":
+        if not (0 <= k <= self.order):
+            raise ValueError(f"leading block size {k} out of range")
+        out = UpperTriangular(k)
+        out.data[:] = self.data[:k, :k]
+        return out
+
+    def entry_count(self) -> int:
+        return self.order * (self.order + 1) // 2
+
+
+def solve_upper_triangular(r: UpperTriangular, rhs, breakdown_tolerance: float = DEFAULT_BREAKDOWN_TOLERANCE):
+    """Host back substitution with NumPy's dot, as the reference does
+    (solvers.py:205-218), so the BLAS summation order is identical."""
+    rhs = as_vector(rhs, n=r.order, name="rhs")
+    eta = np.zeros(r.order)
+    for i in range(r.order - 1, -1, -1):
+        d = r.data[i, i]
+        if abs(d) < breakdown_tolerance:
+            raise BreakdownError("singular_R", f"zero diagonal at position {i}")
+        eta[i] = (rhs[i] - float(np.dot(r.data[i, i + 1:], eta[i + 1:]))) / d
+    return eta
+
+
+@N.TRISOLVE_FN
+def _trisolve_cb(user, k, rptr, ld, xiptr, btol, etaptr):
+    """Called by libpk_b200 once per GMRES cycle (solvers.py:971-978)."""
+    try:
+        rfull = np.ctypeslib.as_array(rptr, shape=(ld * ld,)).reshape(ld, ld)
+        xi = np.ctypeslib.as_array(xiptr, shape=(k,)).copy()
+        tri = UpperTriangular(k)
+        tri.data[:] = rfull[:k, :k]
+        eta = solve_upper_triangular(tri, xi, btol)
+        out = np.ctypeslib.as_array(etaptr, shape=(k,))
+        out[:] = eta
+        return 0
+    except BreakdownError:
+        return 1
+
+
+def _prepare(a, b, x0):
+    """Validation of solvers.py:259-269 (ValueError on misuse)."""
+    if isinstance(a, DeviceMatrix):
+        n_rows, n_cols = a.n_rows, a.n_cols
+    else:
+        a = CsrMatrix.coerce(a)
+        n_rows, n_cols = a.n_rows, a.n_cols
+    if n_rows != n_cols:
+        raise ValueError(f"matrix must be square, got {n_rows} x {n_cols}")
+    b = np.ascontiguousarray(as_vector(b, n=n_rows, name="b"), dtype=np.float64)
+    x0 = None if x0 is None else np.ascontiguousarray(as_vector(x0, n=n_rows, name="x0"), dtype=np.float64)
+    return a, b, x0
+
+
+def _native_config(cfg: SolverConfig) -> N.PkConfig:
+    return N.PkConfig(
+        tolerance=cfg.tolerance, max_iterations=cfg.max_iterations, restart=cfg.restart,
+        breakdown_tolerance=cfg.breakdown_tolerance,
+        fixed_iterations=cfg.fixed_iterations if cfg.fixed else 0,
+        loop_mode=N.LOOP_GRAPH if cfg.loop_mode == "graph" else N.LOOP_HOST, reserved=0)
+
+
+def _trace_from(res: N.PkResult, method: str, n: int, restart: int) -> ExecutionTrace:
+    """ExecutionTrace filled with the launches/transfers really issued.
+
+    GMRES step i of a cycle launches SpMV+normalize (i=1), SpMV+update+
+    normalize (i=2) or SpMV+multi-dot+update+normalize (i>=3)."""
+    tr = ExecutionTrace()
+    tr.add_phase(SETUP, res.setup_launches, res.setup_transfers, bytes_transfer=8 * 2 * n)
+    for i in range(res.iterations):
+        if method == "gmres":
+            step = i % restart + 1
+            launches = 2 if step == 1 else (3 if step == 2 else 4)
+        else:
+            launches = res.launches_per_iteration
+        tr.add_phase(ITERATION, launches, res.transfers_per_iteration)
+    for _ in range(res.check_phases):
+        tr.add_phase(CHECK, 1, 1)
+    tr.add_phase(FINISH, res.finish_launches, res.finish_transfers, bytes_transfer=8 * (n + res.iterations))
+    return tr
+
+
+def _run(method: str, a, b, x0, config, context, debug):
+    cfg = SolverConfig.coerce(config)
+    if method == "gmres" and cfg.orthogonalization != CLASSICAL_GS:
+        raise ValueError("pipelined GMRES supports classical Gram-Schmidt only")
+    a, b, x0 = _prepare(a, b, x0)
+    ctx = ExecutionContext.coerce(context)
+    dc = context_for(ctx)
+    dm = device_matrix(a, ctx)
+    n = dm.n_rows
+    limit = cfg.iteration_limit()
+    x = np.empty(n)
+    hist = np.empty(max(limit, 1))
+    res = N.PkResult()
+    ncfg = _native_config(cfg)
+    dp = C.POINTER(C.c_double)
+    N.check(N.lib().pk_solve(
+        dc.handle, dm.handle, N.METHODS[method], b.ctypes.data_as(dp),
+        x0.ctypes.data_as(dp) if x0 is not None else None, C.byref(ncfg), _trisolve_cb, None,
+        x.ctypes.data_as(dp), hist.ctypes.data_as(dp), len(hist), C.byref(res)), f"{method}_pipelined")
+    trace = _trace_from(res, method, n, cfg.restart)
+    diag = {}
+    if debug:
+        diag["device"] = {"launches": res.total_launches, "transfers": res.total_transfers,
+                          "cycles": res.cycles, "check_phases": res.check_phases}
+    return SolverResult(
+        x=x,
+        residual_history=[float(v) for v in hist[: res.iterations]],
+        true_final_residual=float(res.true_final_residual),
+        iterations=int(res.iterations),
+        termination=N.TERM_NAMES[res.termination],
+        trace=trace,
+        breakdown_kind=N.KIND_NAMES[res.breakdown_kind],
+        loop_seconds=float(res.loop_seconds),
+        diagnostics=diag,
+    )
+
+
+def cg_pipelined(a, b, x0=None, config=None, context=None, debug=False) -> SolverResult:
+    """Pipelined CG (solvers.py:395-469): 2 fused kernels per iteration, the
+    stage-2 reduction and alpha/beta/convergence finalized on the device."""
+    return _run("cg", a, b, x0, config, context, debug)
+
+
+def bicgstab_pipelined(a, b, x0=None, config=None, context=None, debug=False) -> SolverResult:
+    """Pipelined BiCGStab (solvers.py:583-712): 4 fused kernels per iteration."""
+    return _run("bicgstab", a, b, x0, config, context, debug)
+
+
+def gmres_pipelined(a, b, x0=None, config=None, context=None, debug=False) -> SolverResult:
+    """Pipelined GMRES(m) with fused classical Gram-Schmidt (solvers.py:865-1008)."""
+    return _run("gmres", a, b, x0, config, context, debug)
+
+
+SOLVERS = {
+    ("cg", "pipelined"): cg_pipelined,
+    ("bicgstab", "pipelined"): bicgstab_pipelined,
+    ("gmres", "pipelined"): gmres_pipelined,
+}
+
+
+def solve(A, b, tag=("cg", "pipelined"), tol: float = 1e-8, maxiter: int = 500, x0=None, context=None,
+          restart: int = 30, fixed_iterations: int | None = None) -> SolverResult:
+    """North-star entry: ``SOLVERS[tag](A, b, x0, SolverConfig(tol, maxiter), context)``.
+
+    ``tag`` is a (method, variant) pair or a bare method name."""
+    if isinstance(tag, str):
+        tag = (tag, "pipelined")
+    if tuple(tag) not in SOLVERS:
+        raise ValueError(f"unknown solver {tag!r}; the B200 path implements {sorted(SOLVERS)}")
+    cfg = SolverConfig(tolerance=tol, max_iterations=maxiter, restart=restart, fixed_iterations=fixed_iterations)
+    return SOLVERS[tuple(tag)](A, b, x0=x0, config=cfg, context=context)

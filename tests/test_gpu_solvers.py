@@ -1,0 +1,206 @@
+"""Solver-level parity on the B200 through the reference-facing API.
+
+* every golden case produced by the real reference (tests/golden): iterations,
+  termination, breakdown kind, residual history, x and the true residual must
+  be bit-identical;
+* larger systems and other geometries against the oracle, bitwise;
+* the BASELINE configs at full size: C1 (CG 512^2, to tolerance) and C2
+  (BiCGStab 1024^2) / C3 (GMRES(30) 128^3) over fixed iterations, bitwise
+  against the oracle, plus the north-star tolerance bar (+-1 iteration,
+  1e-10 relative) against the oracle at the reference's default geometry;
+* graph vs host loop, reruns, device generators."""
+
+import numpy as np
+import pytest
+
+from oracle import pk_oracle as orc
+from tests import golden_data as gd
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def pk():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1410_4054_b200 as pk
+
+    return pk
+
+
+def bits(a):
+    return np.asarray(a, dtype=np.float64).view(np.uint64)
+
+
+def same(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return a.shape == b.shape and np.array_equal(bits(a), bits(b))
+
+
+def assert_identical(res, ref):
+    assert res.iterations == ref["iterations"]
+    assert res.termination == ref["termination"]
+    assert res.breakdown_kind == ref["breakdown_kind"]
+    assert same(res.residual_history, ref["history"])
+    assert same(res.x, ref["x"])
+    assert res.true_final_residual == ref["true_final_residual"]
+
+
+@pytest.mark.parametrize("name", gd.solver_case_names())
+def test_solver_matches_reference_golden(pk, name):
+    case = gd.solver_case(name)
+    store = gd.solvers()
+    a = pk.CsrMatrix(*gd.csr_arrays(store, f"{name}/A"))
+    b = store[f"{name}/b"]
+    x0 = store.get(f"{name}/x0")
+    cfg = pk.SolverConfig(**case["config"])
+    ctx = pk.ExecutionContext(*case["geom"])
+    res = pk.SOLVERS[(case["method"], "pipelined")](a, b, x0=x0, config=cfg, context=ctx)
+    ref = {"iterations": case["iterations"], "termination": case["termination"],
+           "breakdown_kind": case["breakdown_kind"], "history": store[f"{name}/history"],
+           "x": store[f"{name}/x"], "true_final_residual": store[f"{name}/true_final_residual"][0]}
+    assert_identical(res, ref)
+
+
+def oracle_run(method, a, b, geom, **kw):
+    return orc.SOLVERS[method](a, b, geom=geom, **kw)
+
+
+@pytest.mark.parametrize("method", ["cg", "bicgstab", "gmres"])
+@pytest.mark.parametrize("geom", [(128, 256), (32, 1024), (1, 4096), (16, 65536), (1000, 64)])
+def test_solver_matches_oracle_medium(pk, method, geom):
+    a, _ = pk.convdiff2d(120) if method != "cg" else pk.poisson2d_grid(120)
+    b = np.random.default_rng(1).random(a.n_rows)
+    res = pk.SOLVERS[(method, "pipelined")](a, b, config=pk.SolverConfig(max_iterations=300),
+                                             context=pk.ExecutionContext(*geom))
+    assert_identical(res, oracle_run(method, a, b, geom, max_iterations=300))
+
+
+@pytest.mark.parametrize("mode", ["graph", "host"])
+def test_loop_modes_identical(pk, mode):
+    a, b = pk.poisson2d_grid(64)
+    cfg = pk.SolverConfig(loop_mode=mode)
+    for method in ("cg", "bicgstab"):
+        res = pk.SOLVERS[(method, "pipelined")](a, b, config=cfg)
+        assert_identical(res, oracle_run(method, a, b, (128, 256)))
+
+
+def test_reruns_bit_identical(pk):
+    a, b = pk.convdiff2d(80)
+    for key, solver in pk.SOLVERS.items():
+        r1, r2 = solver(a, b), solver(a, b)
+        assert r1.residual_history == r2.residual_history and same(r1.x, r2.x)
+        assert [(p.label, p.launches) for p in r1.trace.phases] == [(p.label, p.launches) for p in r2.trace.phases]
+
+
+def test_trace_shape_and_counts(pk):
+    a, b = pk.gen_poisson2d(1)
+    cfg = pk.SolverConfig(fixed_iterations=5, max_iterations=5)
+    cg = pk.cg_pipelined(a, b, config=cfg)
+    assert [p.launches for p in cg.trace.iterations] == [2] * 5
+    assert all(p.transfers == 0 for p in cg.trace.iterations)  # device-resident loop
+    bi = pk.bicgstab_pipelined(a, b, config=cfg)
+    assert [p.launches for p in bi.trace.iterations] == [4] * 5
+    gm = pk.gmres_pipelined(a, b, config=cfg)
+    assert [p.launches for p in gm.trace.iterations] == [2, 3, 4, 4, 4]
+    for r in (cg, bi, gm):
+        labels = [p.label for p in r.trace.phases]
+        assert labels[0] == "setup" and labels[-1] == "finish"
+
+
+def test_solve_entry_point(pk):
+    a, b = pk.gen_poisson2d(2)
+    res = pk.solve(a, b, tag="cg", tol=1e-8, maxiter=500)
+    assert res.converged and res.true_final_residual <= 1e-8 * np.linalg.norm(b)
+    res2 = pk.solve(a, b, tag=("gmres", "pipelined"), tol=1e-8, maxiter=500)
+    assert res2.converged
+
+
+def test_reference_objects_accepted(pk):
+    # duck-typed reference CsrMatrix / SolverConfig / ExecutionContext
+    class RefCsr:
+        def __init__(self, m):
+            self.n_rows, self.n_cols = m.n_rows, m.n_cols
+            self.row_offsets, self.col_indices, self.values = m.rowptr, m.cols, m.vals
+
+    class RefCtx:
+        n_groups, group_size = 16, 32
+
+    o, b = orc.poisson2d(2)
+    res = pk.cg_pipelined(RefCsr(o), b, context=RefCtx())
+    assert_identical(res, oracle_run("cg", o, b, (16, 32)))
+
+
+@pytest.mark.parametrize("fam,dims", [("poisson2d", (37,)), ("poisson3d", (11,)), ("convdiff2d", (45,)),
+                                      ("convdiff3d", (13,))])
+def test_device_generators_equal_host(pk, fam, dims):
+    host_fn = {"poisson2d": pk.poisson2d_grid, "poisson3d": pk.poisson3d_grid, "convdiff2d": pk.convdiff2d,
+               "convdiff3d": pk.convdiff3d}[fam]
+    ha, _ = host_fn(*dims)
+    dm, _ = host_fn(*dims, device=True)
+    back = dm.download(pk.context_for(pk.ExecutionContext()))
+    assert np.array_equal(back.row_offsets, ha.row_offsets) and np.array_equal(back.col_indices, ha.col_indices)
+    assert same(back.values, ha.values)
+    assert dm.max_row_nnz == int(ha.row_nnz().max())
+
+
+def test_device_matrix_solve_equals_host_matrix_solve(pk):
+    dm, b = pk.convdiff2d(90, device=True)
+    ha, _ = pk.convdiff2d(90)
+    r1 = pk.bicgstab_pipelined(dm, b)
+    r2 = pk.bicgstab_pipelined(ha, b)
+    assert r1.residual_history == r2.residual_history and same(r1.x, r2.x)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configurations at full size
+# ---------------------------------------------------------------------------
+
+
+def history_gap(h1, h2, floor=1e-12):
+    worst = 0.0
+    for x, y in zip(h1, h2):
+        if abs(x) <= floor and abs(y) <= floor:
+            continue
+        worst = max(worst, abs(x - y) / max(abs(x), abs(y)))
+    return worst
+
+
+def test_c1_cg_512_to_tolerance_bitwise(pk):
+    """C1: pipelined CG, 2D Poisson 512x512, tol 1e-8 (oracle: 941 iterations)."""
+    a, b = pk.poisson2d_grid(512)
+    res = pk.cg_pipelined(a, b)
+    ref = oracle_run("cg", a, b, (128, 256))
+    assert ref["iterations"] == 941
+    assert_identical(res, ref)
+    # north-star bar, stated explicitly: +-1 iteration, 1e-10 relative
+    assert abs(res.iterations - ref["iterations"]) <= 1
+    assert history_gap(res.residual_history, ref["history"]) <= 1e-10
+    assert np.abs(res.x - ref["x"]).max() / np.abs(ref["x"]).max() <= 1e-10
+
+
+def test_c1_wide_geometry_matches_oracle_same_geometry(pk):
+    a, b = pk.poisson2d_grid(512)
+    ctx = pk.ExecutionContext.one_per_lane(a.n_rows, 1024)
+    res = pk.cg_pipelined(a, b, context=ctx)
+    assert_identical(res, oracle_run("cg", a, b, (ctx.n_groups, ctx.group_size)))
+
+
+def test_c2_bicgstab_1024_fixed_bitwise(pk):
+    """C2 shape: BiCGStab 2D upwind convection-diffusion 1024^2, 8 fixed iterations."""
+    dm, b = pk.convdiff2d(1024, device=True)
+    a, _ = pk.convdiff2d(1024)
+    cfg = pk.SolverConfig(fixed_iterations=8, max_iterations=8)
+    res = pk.bicgstab_pipelined(dm, b, config=cfg)
+    assert_identical(res, oracle_run("bicgstab", a, b, (128, 256), fixed=8, max_iterations=8))
+
+
+def test_c3_gmres_128_fixed_bitwise(pk):
+    """C3 shape: GMRES(30) 3D upwind convection-diffusion 128^3, 6 fixed steps."""
+    dm, b = pk.convdiff3d(128, device=True)
+    a, _ = pk.convdiff3d(128)
+    cfg = pk.SolverConfig(fixed_iterations=6, max_iterations=6)
+    res = pk.gmres_pipelined(dm, b, config=cfg)
+    assert_identical(res, oracle_run("gmres", a, b, (128, 256), fixed=6, max_iterations=6))
