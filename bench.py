@@ -1,0 +1,288 @@
+"""Benchmark of the B200 pipelined Krylov path (contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the single-B200 headline): pipelined
+BiCGStab on the 2D first-order upwind convection-diffusion operator, 1024 x
+1024 grid (n = 1 048 576, nnz = 5 238 784), fp64, reference default reduction
+geometry 128 x 256 (bit-identical to the reference CPU implementation at that
+geometry).  A "step" is one pipelined BiCGStab iteration (4 fused kernels);
+the K timed steps are one fixed-iteration device loop (conditional-WHILE CUDA
+graph) timed with CUDA events on its stream, setup excluded -- the paper's /
+reference's loop_seconds protocol (solvers.py:632-695).
+
+value    = time per iteration (us), max over ranks (N > 1: independent
+           replicas, the path does not shard).
+e2e      = the same metric through the public reference-facing call
+           bicgstab_pipelined(A, b, config) with host b in / host x out,
+           per-iteration wall time of the whole call (H2D b, setup, loop,
+           true residual, D2H x + history).
+roofline = dominant kernel (SpMV fused with 3 dots, As = A s), CUDA-event
+           timed alone with an L2 flush between launches, against the
+           measured HBM copy peak (MEASURED_PEAKS.json).
+cpu_baseline / --impl reference = the oracle port of the reference's
+           pipelined BiCGStab (NumPy, single thread) on the same system.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "CG/BiCGStab/GMRES time per iteration vs unknowns (fp64); achieved HBM GB/s"
+SIDE = 1024
+GEOM = (128, 256)
+
+
+def peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def b_csr(n, nnz):
+    return 12 * nnz + 4 * (n + 1)
+
+
+class ClockSampler:
+    """NVML SM clock / throttle reasons sampled during the timed region."""
+
+    BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+           "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(0.002)
+
+    def sample(self):
+        if self.nv is None:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            pass
+
+    def __enter__(self):
+        self.sample()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self.t.join()
+        self.sample()
+
+    def summary(self):
+        if self.nv is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        reasons = [k for k, bit in self.BAD.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_reference(iters, sample_note):
+    """Oracle port (NumPy) of the reference pipelined BiCGStab, 1 thread."""
+    from oracle import pk_oracle as orc
+
+    a, b = orc.convdiff2d(SIDE)
+    timing = {}
+    orc.bicgstab_pipelined(a, b, fixed=iters, max_iterations=iters, geom=GEOM, timing=timing)
+    us = timing["loop_seconds"] / iters * 1e6
+    return {"value": us, "unit": "us/iter", "cores": 1, "kind": "port",
+            "sample": sample_note.format(iters=iters)}
+
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    iters = max(1, min(args.steps, 60))
+    for _ in range(min(args.warmup, 1)):
+        cpu_reference(1, "")
+    cb = cpu_reference(iters, "pipelined BiCGStab convdiff2d 1024^2, {iters} fixed iterations, loop time only "
+                              "(oracle NumPy port of pipekrylov; reference itself is Python and absent on the box)")
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "us/iter",
+            "n_gpus": args.gpus, "steps": iters, "warmup": args.warmup, "ms_per_step": cb["value"] / 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(),
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "us/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def config_block():
+    return {"workload": "pipelined BiCGStab, 2D upwind convection-diffusion 1024x1024 (configs[1])",
+            "n": SIDE * SIDE, "nnz": 5 * SIDE * SIDE - 4 * SIDE, "reduction_geometry": f"{GEOM[0]}x{GEOM[1]}",
+            "parallelism": "replicas", "l2": "working set 131 MB > 126 MB L2; roofline kernel timed with an "
+                                              "L2 flush between launches"}
+
+
+def kernel_roofline(pk, dm, ctx, torch, reps=20):
+    """Dominant kernel: As = A s fused with {As.s, As.As, As.r0*}."""
+    from paper_1410_4054_b200 import fused
+
+    n = dm.n_rows
+    s = torch.rand(n, dtype=torch.float64, device="cuda")
+    r0 = torch.rand(n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    for _ in range(3):
+        fused.spmv_fused(dm, s, ("input", "result", r0), ctx)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fused.spmv_fused(dm, s, ("input", "result", r0), ctx)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    t = statistics.median(times)
+    alg = b_csr(n, dm.nnz) + 24 * n
+    peak, kind = peaks()
+    ach = alg / t / 1e9
+    return {"bound": "hbm", "kernel": "spmv_fused (As = A s; 3 dots)", "achieved": round(ach, 1),
+            "peak": peak, "peak_kind": kind, "unit": "GB/s", "frac": round(ach / peak, 4),
+            "traffic": None, "bytes_per_launch": alg, "us_per_launch": round(t * 1e6, 2)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+
+    import paper_1410_4054_b200 as pk
+    from paper_1410_4054_b200.solvers import solve_resident
+
+    dev = torch.cuda.current_device()
+    ctx = pk.ExecutionContext(*GEOM, device=dev)
+    dm, b_host = pk.convdiff2d(SIDE, device=True, context=ctx)
+    n, nnz = dm.n_rows, dm.nnz
+    b = torch.from_numpy(b_host).to("cuda")
+
+    # warm-up: graph build/instantiate paths, clocks up
+    solve_resident("bicgstab", dm, b, config=pk.SolverConfig(fixed_iterations=args.warmup,
+                                                                max_iterations=args.warmup), context=ctx)
+    cfg = pk.SolverConfig(fixed_iterations=args.steps, max_iterations=args.steps)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        _, res = solve_resident("bicgstab", dm, b, config=cfg, context=ctx)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    loop_s = res.loop_seconds
+    if dist:
+        t = torch.tensor([loop_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        loop_s = float(t.item())
+    us_iter = loop_s / args.steps * 1e6
+    iter_bytes = 2 * b_csr(n, nnz) + 144 * n
+    peak, peak_kind = peaks()
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    roof = kernel_roofline(pk, dm, ctx, torch)
+
+    # e2e through the public API: host b in, host x + history out
+    a_host, _ = pk.convdiff2d(SIDE)
+    e2e_iters = min(args.steps, 200)
+    ecfg = pk.SolverConfig(fixed_iterations=e2e_iters, max_iterations=e2e_iters)
+    pk.bicgstab_pipelined(a_host, b_host, config=ecfg, context=ctx)  # uploads A once (cached on A)
+    walls = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = pk.bicgstab_pipelined(a_host, b_host, config=ecfg, context=ctx)
+        walls.append(time.perf_counter() - t0)
+    e2e_us = statistics.median(walls) / e2e_iters * 1e6
+
+    line = {
+        "metric": METRIC,
+        "value": round(us_iter, 3),
+        "unit": "us/iter",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(us_iter / 1e3, 6),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": config_block(),
+        "iteration_roofline": {"bytes_per_iteration": iter_bytes,
+                               "achieved_gbs": round(iter_bytes / (us_iter * 1e-6) / 1e9, 1),
+                               "frac": round(iter_bytes / (us_iter * 1e-6) / 1e9 / peak, 4)},
+        "roofline": roof,
+        "e2e": {"value": round(e2e_us, 3), "unit": "us/iter", "iterations_per_call": e2e_iters,
+                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 8 * e2e_iters},
+        "gpu_launches": int(res.diagnostics.get("launches_per_iteration", 4)) * args.steps,
+        "clocks": clk.summary(),
+        "termination": res.termination,
+    }
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_reference(
+            40, "pipelined BiCGStab convdiff2d 1024^2, {iters} fixed iterations, loop time only (oracle NumPy port)")
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -123,9 +123,11 @@ int pk_device_count(int* count);
  * power of two.  Creates a non-blocking stream on `device`. */
 int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, pk_ctx** out);
 int pk_ctx_destroy(pk_ctx* ctx);
-/* Use an external stream (cudaStream_t) for kernel-level entries; NULL
- * restores the context's own stream. */
+/* Run kernel-level entries on `stream` (a cudaStream_t; NULL is the legacy
+ * default stream, as everywhere in CUDA).  pk_ctx_reset_stream restores the
+ * context's private non-blocking stream. */
 int pk_ctx_set_stream(pk_ctx* ctx, void* stream);
+int pk_ctx_reset_stream(pk_ctx* ctx);
 int pk_ctx_synchronize(pk_ctx* ctx);
 int pk_ctx_geometry(const pk_ctx* ctx, int64_t* n_groups, int64_t* group_size);
 

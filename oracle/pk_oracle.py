@@ -30,6 +30,7 @@ round to nearest, never fused):
 from __future__ import annotations
 
 import math
+import time
 
 import numpy as np
 
@@ -268,7 +269,7 @@ def _setup(a, b, x0):
 
 
 def cg_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None,
-                 geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL):
+                 geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL, timing=None):
     """Restatement of solvers.cg_pipelined (solvers.py:395-469)."""
     a, b, x = _setup(a, b, x0)
     lbt = 0.0 if fixed else btol  # solvers.py:141-145
@@ -288,6 +289,7 @@ def cg_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None,
     alpha = rr / pap
     beta = alpha * alpha * apap / rr - 1.0
     term, kind = MAX_ITER, None
+    t0 = time.perf_counter()  # loop_seconds protocol, solvers.py:444/468
     for _ in range(limit):
         rr_part = cg_update(x, r, p, ap, alpha, beta, geom)
         ap, pq = spmv_fused(a, p, ("input", "result"), geom)
@@ -307,11 +309,13 @@ def cg_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None,
             break
         alpha = rr / pap
         beta = alpha * alpha * apap / rr - 1.0
+    if timing is not None:
+        timing["loop_seconds"] = time.perf_counter() - t0
     return _finish(a, b, x, geom, hist, term, kind)
 
 
 def bicgstab_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None,
-                       geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL):
+                       geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL, timing=None):
     """Restatement of solvers.bicgstab_pipelined (solvers.py:583-712)."""
     a, b, x = _setup(a, b, x0)
     lbt = 0.0 if fixed else btol
@@ -328,6 +332,7 @@ def bicgstab_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None,
         return _finish(a, b, x, geom, hist, CONVERGED, None)
     term, kind, half = MAX_ITER, None, None
     it = 0
+    t0 = time.perf_counter()  # solvers.py:632/695
     while it < limit:
         it += 1
         confirm = False
@@ -374,13 +379,15 @@ def bicgstab_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None,
         if confirm and _true_residual(a, b, x, geom) <= tol * scale:
             term = CONVERGED
             break
+    if timing is not None:
+        timing["loop_seconds"] = time.perf_counter() - t0
     if half is not None:
         x += half * p
     return _finish(a, b, x, geom, hist, term, kind)
 
 
 def gmres_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None, restart=30,
-                    geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL):
+                    geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL, timing=None):
     """Restatement of solvers.gmres_pipelined (solvers.py:865-1008)."""
     a, b, x = _setup(a, b, x0)
     lbt = 0.0 if fixed else btol
@@ -404,6 +411,7 @@ def gmres_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None, res
         basis, xi_parts = [], []
         rmat = np.zeros((m, m))
         lucky = False
+        t0 = time.perf_counter()  # inner loop only, solvers.py:928/953
         while len(basis) < m and total < limit:
             i = len(basis) + 1
             if i == 1:
@@ -422,6 +430,8 @@ def gmres_pipelined(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None, res
             basis.append(w)
             xi_parts.append(xi_part)
             total += 1
+        if timing is not None:
+            timing["loop_seconds"] = timing.get("loop_seconds", 0.0) + time.perf_counter() - t0
         k = len(basis)
         conv_at = None
         gate = None

@@ -74,6 +74,7 @@ SIGNATURES = {
     "pk_ctx_create": [C.c_int, C.c_int64, C.c_int64, C.POINTER(_P)],
     "pk_ctx_destroy": [_P],
     "pk_ctx_set_stream": [_P, _P],
+    "pk_ctx_reset_stream": [_P],
     "pk_ctx_synchronize": [_P],
     "pk_ctx_geometry": [_P, _I64P, _I64P],
     "pk_csr_upload": [_P, C.c_int64, C.c_int64, _I64P, _I64P, _DP, C.POINTER(_P)],

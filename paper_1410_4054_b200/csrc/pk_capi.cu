@@ -83,13 +83,13 @@ static int set_device(int dev) {
 
 template <int NQ, int U, class Op>
 __global__ void __launch_bounds__(256) k_reduce(Geom geo, Op op, ScalarPtrs sp, double* part, int ld,
-                                                int col0, SolveState* st, int gate,
+                                                int col0, int nstore, SolveState* st, int gate,
                                                 const int32_t* skip, int fin, int fin_arg) {
   extern __shared__ double smem[];
   if (skip && *(volatile const int32_t*)skip) return;
   if (st && !gate_open(st, gate)) return;
   op.scalars(sp);
-  stage1_all_groups<NQ, U>(geo, op, smem, part, ld, col0);
+  stage1_all_groups<NQ, U>(geo, op, smem, part, ld, col0, nstore);
   if (fin != FIN_NONE && st) {
     if (elect_last_block(&st->ticket)) finalize(st, fin, fin_arg);
   }
@@ -267,15 +267,17 @@ static int grid_elem(const pk_ctx* c, int64_t n, int block) {
 template <int NQ, int U, class Op>
 static int launch_reduce(const pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp,
                          double* part, int ld, int col0, SolveState* st = nullptr, int gate = GATE_NONE,
-                         const int32_t* skip = nullptr, int fin = FIN_NONE, int fin_arg = 0) {
+                         const int32_t* skip = nullptr, int fin = FIN_NONE, int fin_arg = 0,
+                         int nstore = NQ) {
   Geom geo = make_geom(n, c->ng, c->gs, 256);
   size_t smem = engine_smem_bytes(geo, NQ);
   auto kern = k_reduce<NQ, U, Op>;
-  if (smem > 48 * 1024) {
-    if (smem > 227 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
+  if (smem > 32 * 1024) {  // dynamic + static (finalizer scratch) must fit the opt-in limit
+    if (smem > 220 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
     PK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
-  kern<<<grid_for(c, c->ng), geo.T, smem, s>>>(geo, op, sp, part, ld, col0, st, gate, skip, fin, fin_arg);
+  kern<<<grid_for(c, c->ng), geo.T, smem, s>>>(geo, op, sp, part, ld, col0, nstore, st, gate, skip, fin,
+                                                fin_arg);
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
@@ -375,14 +377,14 @@ static int multidot_t(const pk_ctx* c, cudaStream_t s, int64_t n, int nb, const 
   op.nb = nb;
   for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
   constexpr int U = NB <= 2 ? 4 : (NB <= 8 ? 2 : 1);
-  return launch_reduce<NB, U>(c, s, n, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
+  return launch_reduce<NB, U>(c, s, n, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg, nb);
 }
 
 // Largest NB whose leaf stack fits in shared memory for this geometry.
 static int multidot_nb_cap(const pk_ctx* c, int64_t n) {
   Geom geo = make_geom(n, c->ng, c->gs, 256);
   for (int nb : {32, 16, 8, 4, 2, 1}) {
-    if (engine_smem_bytes(geo, nb) <= 200 * 1024) return nb;
+    if (engine_smem_bytes(geo, nb) <= 192 * 1024) return nb;
   }
   return 1;
 }
@@ -499,7 +501,13 @@ extern "C" int pk_ctx_destroy(pk_ctx* c) {
 
 extern "C" int pk_ctx_set_stream(pk_ctx* c, void* stream) {
   if (!c) return fail(PK_ERR_INVALID, "ctx is NULL");
-  c->stream = stream ? (cudaStream_t)stream : c->own;
+  c->stream = (cudaStream_t)stream;  // NULL: legacy default stream
+  return PK_OK;
+}
+
+extern "C" int pk_ctx_reset_stream(pk_ctx* c) {
+  if (!c) return fail(PK_ERR_INVALID, "ctx is NULL");
+  c->stream = c->own;
   return PK_OK;
 }
 

@@ -187,20 +187,20 @@ __device__ __forceinline__ void run_group(const Geom& geo, int g, Op& op, double
 }
 
 // Full stage-1 over all groups handled by this CTA; writes
-// part[g * ld + col0 + q].  Returns after the CTA's last group.
+// part[g * ld + col0 + q] for q < nstore.  Returns after the CTA's last group.
 template <int NQ, int U, class Op>
 __device__ __forceinline__ void stage1_all_groups(const Geom& geo, Op& op, double* smem,
-                                                  double* part, int ld, int col0) {
+                                                  double* part, int ld, int col0, int nstore) {
   for (int g = blockIdx.x; g < geo.n_groups; g += gridDim.x) {
     double lane[NQ];
     run_group<NQ, U>(geo, g, op, smem, lane);
-    if ((int)threadIdx.x < geo.T) {
-      // threads beyond T do not exist (blockDim == T)
-    }
     block_tree<NQ>(lane, smem, geo.T);
     if (threadIdx.x == 0 && part) {
+      // only the nstore live quantities: templates padded to NQ (e.g. a
+      // multi-dot over nb < NB vectors) must not spill into other columns
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) part[(int64_t)g * ld + col0 + q] = lane[q];
+      for (int q = 0; q < NQ; ++q)
+        if (q < nstore) part[(int64_t)g * ld + col0 + q] = lane[q];
     }
     __syncthreads();  // smem (tree + stack) reused by the next group
   }

@@ -30,10 +30,14 @@ class DeviceContext:
         self.handle = h
 
     def set_stream(self, stream) -> None:
-        """Run kernel-level entries on ``stream`` (a torch.cuda.Stream, raw
-        cudaStream_t int, or None for the context's own stream)."""
+        """Run kernel-level entries on ``stream``: a torch.cuda.Stream or a raw
+        cudaStream_t int (0 = the legacy default stream, torch's default)."""
         ptr = getattr(stream, "cuda_stream", stream)
-        N.check(N.lib().pk_ctx_set_stream(self.handle, C.c_void_p(ptr) if ptr else None))
+        N.check(N.lib().pk_ctx_set_stream(self.handle, C.c_void_p(int(ptr)) if ptr else None))
+
+    def reset_stream(self) -> None:
+        """Back to the context's private non-blocking stream."""
+        N.check(N.lib().pk_ctx_reset_stream(self.handle))
 
     def synchronize(self) -> None:
         N.check(N.lib().pk_ctx_synchronize(self.handle))

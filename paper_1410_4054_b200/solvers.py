@@ -228,6 +228,7 @@ def _run(method: str, a, b, x0, config, context, debug):
     res = N.PkResult()
     ncfg = _native_config(cfg)
     dp = C.POINTER(C.c_double)
+    dc.reset_stream()
     N.check(N.lib().pk_solve(
         dc.handle, dm.handle, N.METHODS[method], b.ctypes.data_as(dp),
         x0.ctypes.data_as(dp) if x0 is not None else None, C.byref(ncfg), _trisolve_cb, None,
@@ -284,3 +285,42 @@ def solve(A, b, tag=("cg", "pipelined"), tol: float = 1e-8, maxiter: int = 500, 
         raise ValueError(f"unknown solver {tag!r}; the B200 path implements {sorted(SOLVERS)}")
     cfg = SolverConfig(tolerance=tol, max_iterations=maxiter, restart=restart, fixed_iterations=fixed_iterations)
     return SOLVERS[tuple(tag)](A, b, x0=x0, config=cfg, context=context)
+
+
+def solve_resident(method: str, a, b, x0=None, config=None, context=None):
+    """HBM-resident solve: ``a`` a DeviceMatrix (or CsrMatrix, uploaded once),
+    ``b``/``x0`` float64 CUDA tensors; returns (x tensor, SolverResult without
+    a host copy of x).  No host<->device vector traffic besides the history --
+    the entry the benchmark times (pk_solve_device)."""
+    import torch
+
+    cfg = SolverConfig.coerce(config)
+    if method == "gmres" and cfg.orthogonalization != CLASSICAL_GS:
+        raise ValueError("pipelined GMRES supports classical Gram-Schmidt only")
+    ctx = ExecutionContext.coerce(context)
+    dc = context_for(ctx)
+    dm = device_matrix(a, ctx)
+    n = dm.n_rows
+    if not (isinstance(b, torch.Tensor) and b.is_cuda and b.dtype == torch.float64 and b.shape == (n,)):
+        raise ValueError("b must be a float64 CUDA tensor of length n")
+    b = b.contiguous()
+    x = torch.empty_like(b)
+    hist = np.empty(max(cfg.iteration_limit(), 1))
+    res = N.PkResult()
+    ncfg = _native_config(cfg)
+    x0p = None
+    if x0 is not None:
+        x0 = x0.contiguous()
+        x0p = C.c_void_p(x0.data_ptr())
+    dc.reset_stream()
+    N.check(N.lib().pk_solve_device(
+        dc.handle, dm.handle, N.METHODS[method], C.c_void_p(b.data_ptr()), x0p, C.byref(ncfg), _trisolve_cb,
+        None, C.c_void_p(x.data_ptr()), hist.ctypes.data_as(C.POINTER(C.c_double)), len(hist), C.byref(res)),
+        f"{method}_pipelined")
+    result = SolverResult(
+        x=None, residual_history=[float(v) for v in hist[: res.iterations]],
+        true_final_residual=float(res.true_final_residual), iterations=int(res.iterations),
+        termination=N.TERM_NAMES[res.termination], trace=_trace_from(res, method, n, cfg.restart),
+        breakdown_kind=N.KIND_NAMES[res.breakdown_kind], loop_seconds=float(res.loop_seconds),
+        diagnostics={"launches": res.total_launches, "launches_per_iteration": res.launches_per_iteration})
+    return x, result

@@ -171,8 +171,8 @@ def history_gap(h1, h2, floor=1e-12):
 def test_c1_cg_512_to_tolerance_bitwise(pk):
     """C1: pipelined CG, 2D Poisson 512x512, tol 1e-8 (oracle: 941 iterations)."""
     a, b = pk.poisson2d_grid(512)
-    res = pk.cg_pipelined(a, b)
-    ref = oracle_run("cg", a, b, (128, 256))
+    res = pk.cg_pipelined(a, b, config=pk.SolverConfig(max_iterations=2000))
+    ref = oracle_run("cg", a, b, (128, 256), max_iterations=2000)
     assert ref["iterations"] == 941
     assert_identical(res, ref)
     # north-star bar, stated explicitly: +-1 iteration, 1e-10 relative
@@ -184,8 +184,8 @@ def test_c1_cg_512_to_tolerance_bitwise(pk):
 def test_c1_wide_geometry_matches_oracle_same_geometry(pk):
     a, b = pk.poisson2d_grid(512)
     ctx = pk.ExecutionContext.one_per_lane(a.n_rows, 1024)
-    res = pk.cg_pipelined(a, b, context=ctx)
-    assert_identical(res, oracle_run("cg", a, b, (ctx.n_groups, ctx.group_size)))
+    res = pk.cg_pipelined(a, b, config=pk.SolverConfig(max_iterations=2000), context=ctx)
+    assert_identical(res, oracle_run("cg", a, b, (ctx.n_groups, ctx.group_size), max_iterations=2000))
 
 
 def test_c2_bicgstab_1024_fixed_bitwise(pk):
