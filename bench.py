@@ -4,7 +4,7 @@ Workload (BASELINE.json configs[1], the single-B200 headline): pipelined
 BiCGStab on the 2D first-order upwind convection-diffusion operator, 1024 x
 1024 grid (n = 1 048 576, nnz = 5 238 784), fp64, reference default reduction
 geometry 128 x 256 (bit-identical to the reference CPU implementation at that
-geometry).  A "step" is one pipelined BiCGStab iteration (4 fused kernels);
+geometry).  A "step" is one pipelined BiCGStab iteration (2 fused kernels);
 the K timed steps are one fixed-iteration device loop (conditional-WHILE CUDA
 graph) timed with CUDA events on its stream, setup excluded -- the paper's /
 reference's loop_seconds protocol (solvers.py:632-695).
@@ -15,8 +15,8 @@ e2e      = the same metric through the public reference-facing call
            bicgstab_pipelined(A, b, config) with host b in / host x out,
            per-iteration wall time of the whole call (H2D b, setup, loop,
            true residual, D2H x + history).
-roofline = dominant kernel (SpMV fused with 3 dots, As = A s), CUDA-event
-           timed alone with an L2 flush between launches, against the
+roofline = dominant loop kernel, CUDA-event timed per launch inside a
+           host-enqueued fixed-iteration loop (PK_FLAG_PROFILE), against the
            measured HBM copy peak (MEASURED_PEAKS.json).
 cpu_baseline / --impl reference = the oracle port of the reference's
            pipelined BiCGStab (NumPy, single thread) on the same system.
@@ -140,37 +140,51 @@ def run_reference_arm(args, rank):
 def config_block():
     return {"workload": "pipelined BiCGStab, 2D upwind convection-diffusion 1024x1024 (configs[1])",
             "n": SIDE * SIDE, "nnz": 5 * SIDE * SIDE - 4 * SIDE, "reduction_geometry": f"{GEOM[0]}x{GEOM[1]}",
-            "parallelism": "replicas", "l2": "working set 131 MB > 126 MB L2; roofline kernel timed with an "
-                                              "L2 flush between launches"}
+            "parallelism": "replicas",
+            "l2": "inputs larger than L2 (per-iteration working set: CSR 67 MB + 11 n-vectors of 8.4 MB = 159 MB "
+                  "> 126 MB L2); no flush between iterations"}
 
 
-def kernel_roofline(pk, dm, ctx, torch, reps=20):
-    """Dominant kernel: As = A s fused with {As.s, As.As, As.r0*}."""
-    from paper_1410_4054_b200 import fused
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full capture summary (profiles/), or None."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+def kernel_roofline(pk, dm, ctx, torch, b, iters=200):
+    """Per-kernel CUDA-event times of the two loop kernels (host-enqueued
+    loop with PK_FLAG_PROFILE, events on the launching stream), against the
+    measured HBM copy peak.  Algorithmic bytes per launch (int32 indices,
+    fp64 values, every vector read/written once):
+      As-SpMV  (OpBicgB): B_CSR + 32 n   (read r, Ap, r0*; write As)
+      xrp+Ap   (OpBicgA): B_CSR + 80 n   (read x, r, p, Ap, As, r0*; write x, r, p, Ap)"""
+    from paper_1410_4054_b200.solvers import solve_resident
 
     n = dm.n_rows
-    s = torch.rand(n, dtype=torch.float64, device="cuda")
-    r0 = torch.rand(n, dtype=torch.float64, device="cuda")
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
-    for _ in range(3):
-        fused.spmv_fused(dm, s, ("input", "result", r0), ctx)
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(reps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        fused.spmv_fused(dm, s, ("input", "result", r0), ctx)
-        e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1) * 1e-3)
-    t = statistics.median(times)
-    alg = b_csr(n, dm.nnz) + 24 * n
+    cfg = pk.SolverConfig(fixed_iterations=iters, max_iterations=iters, loop_mode="host")
+    solve_resident("bicgstab", dm, b, config=cfg, context=ctx, profile=True)  # warm
+    _, res = solve_resident("bicgstab", dm, b, config=cfg, context=ctx, profile=True)
+    ks, kl = res.diagnostics["kernel_seconds"], res.diagnostics["kernel_launches"]
+    bc = b_csr(n, dm.nnz)
+    kernels = [("k_reduce<OpBicgB> (s-update + As = A s + 4 dots)", bc + 32 * n, ks[0], kl[0]),
+               ("k_reduce<OpBicgA> (xrp update + Ap = A p + 2 dots)", bc + 80 * n, ks[1], kl[1])]
     peak, kind = peaks()
-    ach = alg / t / 1e9
-    return {"bound": "hbm", "kernel": "spmv_fused (As = A s; 3 dots)", "achieved": round(ach, 1),
-            "peak": peak, "peak_kind": kind, "unit": "GB/s", "frac": round(ach / peak, 4),
-            "traffic": None, "bytes_per_launch": alg, "us_per_launch": round(t * 1e6, 2)}
+    rows = []
+    for name, alg, sec, cnt in kernels:
+        t = sec / max(cnt, 1)
+        rows.append({"kernel": name, "bytes_per_launch": alg, "launches": cnt, "us_per_launch": round(t * 1e6, 2),
+                     "achieved": round(alg / t / 1e9, 1) if t > 0 else None})
+    dom = max(rows, key=lambda r: r["us_per_launch"])
+    total = sum(r["us_per_launch"] for r in rows)
+    return {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved"], "peak": peak,
+            "peak_kind": kind, "unit": "GB/s", "frac": round(dom["achieved"] / peak, 4),
+            "traffic": ncu_traffic(dom["kernel"].split(" ")[0]), "bytes_per_launch": dom["bytes_per_launch"],
+            "us_per_launch": dom["us_per_launch"], "share_of_step": round(dom["us_per_launch"] / total, 3),
+            "kernels": rows}
 
 
 def main():
@@ -180,6 +194,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--loop", default="graph", choices=["graph", "host"],
+                    help="iteration loop driver (host: per-launch kernels visible to ncu)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -214,7 +230,7 @@ def main():
     # warm-up: graph build/instantiate paths, clocks up
     solve_resident("bicgstab", dm, b, config=pk.SolverConfig(fixed_iterations=args.warmup,
                                                                 max_iterations=args.warmup), context=ctx)
-    cfg = pk.SolverConfig(fixed_iterations=args.steps, max_iterations=args.steps)
+    cfg = pk.SolverConfig(fixed_iterations=args.steps, max_iterations=args.steps, loop_mode=args.loop)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -229,7 +245,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         loop_s = float(t.item())
     us_iter = loop_s / args.steps * 1e6
-    iter_bytes = 2 * b_csr(n, nnz) + 144 * n
+    # algorithmic bytes of the fused 2-kernel iteration (see kernel_roofline)
+    iter_bytes = 2 * b_csr(n, nnz) + 112 * n
     peak, peak_kind = peaks()
 
     if rank != 0:
@@ -237,7 +254,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    roof = kernel_roofline(pk, dm, ctx, torch)
+    roof = kernel_roofline(pk, dm, ctx, torch, b)
 
     # e2e through the public API: host b in, host x + history out
     a_host, _ = pk.convdiff2d(SIDE)
@@ -267,12 +284,14 @@ def main():
         "data": "synthetic",
         "config": config_block(),
         "iteration_roofline": {"bytes_per_iteration": iter_bytes,
+                               "reference_4kernel_bytes": 2 * b_csr(n, nnz) + 144 * n,
                                "achieved_gbs": round(iter_bytes / (us_iter * 1e-6) / 1e9, 1),
                                "frac": round(iter_bytes / (us_iter * 1e-6) / 1e9 / peak, 4)},
         "roofline": roof,
         "e2e": {"value": round(e2e_us, 3), "unit": "us/iter", "iterations_per_call": e2e_iters,
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 8 * e2e_iters},
-        "gpu_launches": int(res.diagnostics.get("launches_per_iteration", 4)) * args.steps,
+        # loop kernels (2 per iteration) + the first As-SpMV and the final update
+        "gpu_launches": int(res.diagnostics.get("launches_per_iteration", 2)) * args.steps,
         "clocks": clk.summary(),
         "termination": res.termination,
     }

@@ -85,8 +85,12 @@ typedef struct pk_config {
   double breakdown_tolerance;
   int64_t fixed_iterations;
   int32_t loop_mode;
-  int32_t reserved;
+  int32_t flags;                /* PK_FLAG_* */
 } pk_config;
+
+/* pk_config.flags */
+#define PK_FLAG_PROFILE 1 /* PK_LOOP_HOST only: CUDA-event time of every loop
+                             kernel, returned in pk_result.kernel_* (bench) */
 
 /* SolverResult (solvers.py:148-171) plus real launch/transfer counts for
  * the ExecutionTrace (execmodel.py:110-185). */
@@ -106,6 +110,10 @@ typedef struct pk_result {
   int64_t total_transfers;
   int64_t cycles;               /* GMRES restart cycles */
   int64_t check_phases;         /* BiCGStab true-residual confirmations */
+  /* PK_FLAG_PROFILE: per loop-kernel slot (CG: 0 = fused step; BiCGStab:
+   * 0 = As-SpMV, 1 = xrp+Ap-SpMV) summed event time and launch count */
+  double kernel_seconds[4];
+  int64_t kernel_launches[4];
 } pk_result;
 
 /* GMRES host triangular solve R eta = xi (solvers.py:205-218).  R is the

@@ -21,6 +21,7 @@ METHODS = {"cg": 0, "bicgstab": 1, "gmres": 2}
 DOT_INPUT, DOT_RESULT, DOT_VECTOR = 0, 1, 2
 GEN = {"poisson2d": 0, "poisson3d": 1, "convdiff2d": 2, "convdiff3d": 3}
 LOOP_GRAPH, LOOP_HOST = 0, 1
+FLAG_PROFILE = 1
 
 
 class NativeError(RuntimeError):
@@ -35,7 +36,7 @@ class PkConfig(C.Structure):
         ("breakdown_tolerance", C.c_double),
         ("fixed_iterations", C.c_int64),
         ("loop_mode", C.c_int32),
-        ("reserved", C.c_int32),
+        ("flags", C.c_int32),
     ]
 
 
@@ -56,6 +57,8 @@ class PkResult(C.Structure):
         ("total_transfers", C.c_int64),
         ("cycles", C.c_int64),
         ("check_phases", C.c_int64),
+        ("kernel_seconds", C.c_double * 4),
+        ("kernel_launches", C.c_int64 * 4),
     ]
 
 

@@ -61,6 +61,10 @@ struct pk_ctx {
   SolveState* scratch = nullptr;  // kernel-level finalizer state
   int32_t* scratch_flag = nullptr;
   double* scratch_d = nullptr;
+  double* spill = nullptr;        // engine CHAIN spill, spill_cap doubles
+  size_t spill_cap = 0;
+  unsigned* gtick = nullptr;      // per-group tickets [ng] + global ticket
+  unsigned* ticket = nullptr;
 };
 
 struct pk_mat {
@@ -81,27 +85,30 @@ static int set_device(int dev) {
 // kernels
 // ---------------------------------------------------------------------------
 
-template <int NQ, int U, class Op>
-__global__ void __launch_bounds__(256) k_reduce(Geom geo, Op op, ScalarPtrs sp, double* part, int ld,
-                                                int col0, int nstore, SolveState* st, int gate,
-                                                const int32_t* skip, int fin, int fin_arg) {
+template <int NQ, int U, int MINB, class Op>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_reduce(const __grid_constant__ Geom geo, const __grid_constant__ Op op0, ScalarPtrs sp, double* part, int ld,
+             int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin, int fin_arg) {
   extern __shared__ double smem[];
   if (skip && *(volatile const int32_t*)skip) return;
-  if (st && !gate_open(st, gate)) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  if (st && !gate_open(st, gate, ing)) return;
+  Op op = op0;
   op.scalars(sp);
-  stage1_all_groups<NQ, U>(geo, op, smem, part, ld, col0, nstore);
-  if (fin != FIN_NONE && st) {
-    if (elect_last_block(&st->ticket)) finalize(st, fin, fin_arg);
-  }
+  bool last = engine_run<NQ, U>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+  if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing);
 }
 
-template <int U, class Op>
-__global__ void __launch_bounds__(256) k_sweep(int64_t n, Op op, SolveState* st, int gate) {
-  if (st && !gate_open(st, gate)) return;
-  sweep_all<U>(n, op);
+template <class Op>
+__global__ void __launch_bounds__(kThreads, 3) k_sweep(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
+  extern __shared__ double smem[];
+  if (st && !gate_open(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0)) return;
+  op.scalars(sp);
+  sweep_tiles(n, op, smem);
 }
 
-__global__ void k_finalize(SolveState* st, int fin, int arg) { finalize(st, fin, arg); }
+__global__ void k_finalize(SolveState* st, int fin, int arg) { finalize(st, fin, arg, false); }
 
 // totals[q] = serial sum of column q (reduce_stage2 / in-kernel finalize)
 __global__ void k_stage2(const double* part, int ng, int ld, int nq, double* out) {
@@ -253,9 +260,30 @@ __global__ void k_row_max(const int64_t* counts, int64_t n, unsigned long long* 
 // launch helpers
 // ---------------------------------------------------------------------------
 
-static int grid_for(const pk_ctx* c, int64_t groups) {
-  int64_t cap = (int64_t)c->sm_count * 8;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(groups, cap));
+// Scratch of the engine (CHAIN spill + per-group tickets), sized for nq
+// quantities.  Must be called outside stream capture (it may reallocate).
+static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
+  Geom geo = make_geom(n, c->ng, c->gs);
+  if (geo.leaf) return PK_OK;
+  size_t need = (size_t)geo.G * (size_t)std::max(nq, 1);
+  if (need <= c->spill_cap) return PK_OK;
+  PK_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->spill) cudaFree(c->spill);
+  c->spill = nullptr;
+  c->spill_cap = 0;
+  PK_CUDA(cudaMalloc(&c->spill, need * sizeof(double)));
+  c->spill_cap = need;
+  return PK_OK;
+}
+
+static Scratch scratch_of(const pk_ctx* c) { return Scratch{c->spill, c->gtick, c->ticket}; }
+
+template <class K>
+static int engine_grid(const pk_ctx* c, K kern, size_t smem, int64_t units) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  int64_t cap = (int64_t)c->sm_count * occ;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(units, cap));
 }
 
 static int grid_elem(const pk_ctx* c, int64_t n, int block) {
@@ -265,27 +293,38 @@ static int grid_elem(const pk_ctx* c, int64_t n, int block) {
 }
 
 template <int NQ, int U, class Op>
-static int launch_reduce(const pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp,
+static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp,
                          double* part, int ld, int col0, SolveState* st = nullptr, int gate = GATE_NONE,
                          const int32_t* skip = nullptr, int fin = FIN_NONE, int fin_arg = 0,
                          int nstore = NQ) {
-  Geom geo = make_geom(n, c->ng, c->gs, 256);
-  size_t smem = engine_smem_bytes(geo, NQ);
-  auto kern = k_reduce<NQ, U, Op>;
-  if (smem > 32 * 1024) {  // dynamic + static (finalizer scratch) must fit the opt-in limit
-    if (smem > 220 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
+  Geom geo = make_geom(n, c->ng, c->gs);
+  if (!geo.leaf && (size_t)geo.G * (size_t)nstore > c->spill_cap)
+    return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
+  size_t smem = engine_smem_bytes(geo, NQ, U, Op::kSpmv);
+  constexpr int MINB = NQ > 8 ? 1 : (NQ > 4 ? 2 : Op::kMinBlocks);
+  auto kern = k_reduce<NQ, U, MINB, Op>;
+  if (smem + 1024 > 48 * 1024) {
+    if (smem > 200 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
     PK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
-  kern<<<grid_for(c, c->ng), geo.T, smem, s>>>(geo, op, sp, part, ld, col0, nstore, st, gate, skip, fin,
-                                                fin_arg);
-  PK_CUDA(cudaGetLastError());
+  const int grid = engine_grid(c, kern, smem, geo.units);
+  kern<<<grid, kThreads, smem, s>>>(geo, op, sp, part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin,
+                                    fin_arg);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(PK_ERR_CUDA, std::string("engine launch (nq=") + std::to_string(NQ) + ", smem=" +
+                                 std::to_string(smem) + ", grid=" + std::to_string(grid) + ", leaf=" +
+                                 std::to_string(geo.leaf) + "): " + cudaGetErrorString(e));
   return PK_OK;
 }
 
-template <int U, class Op>
-static int launch_sweep(const pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, SolveState* st = nullptr,
-                        int gate = GATE_NONE) {
-  k_sweep<U, Op><<<grid_elem(c, n, 256), 256, 0, s>>>(n, op, st, gate);
+template <class Op>
+static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp = ScalarPtrs{},
+                        SolveState* st = nullptr, int gate = GATE_NONE) {
+  size_t smem = Op::kSpmv ? (size_t)kWarps * kPCap * sizeof(double) : 0;
+  auto kern = k_sweep<Op>;
+  int64_t tiles = (n + 31) / 32;
+  kern<<<engine_grid(c, kern, smem, (tiles + kWarps - 1) / kWarps), kThreads, smem, s>>>(n, op, sp, st, gate);
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
@@ -295,39 +334,34 @@ static Csr<RowT> csr_of(const pk_mat* a) {
   return Csr<RowT>{(const RowT*)a->rowptr, a->cols, a->vals};
 }
 
-// SpMV with NQ fused dots; dispatch on row index type and register width.
-template <int NQ, typename RowT, int W>
-static int spmv_fused_t(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q,
+// SpMV with NQ fused dots; dispatch on the row index type.
+template <int NQ, typename RowT>
+static int spmv_fused_t(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q,
                         const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
                         SolveState* st, int gate, int fin, int fin_arg) {
-  OpSpmvFused<RowT, W, NQ> op{};
+  OpSpmvFused<RowT, NQ> op{};
   op.A = csr_of<RowT>(a);
   op.p = p;
   op.q = q;
   for (int k = 0; k < 4; ++k) { op.kind[k] = PK_DOT_RESULT; op.w[k] = nullptr; }
   for (int k = 0; k < NQ; ++k) { op.kind[k] = kinds[k]; op.w[k] = w ? w[k] : nullptr; }
-  constexpr int U = W <= 4 ? 4 : 2;
   if constexpr (NQ == 0) {
-    return launch_sweep<U>(c, s, a->n_rows, op, st, gate);
+    return launch_sweep(c, s, a->n_rows, op, ScalarPtrs{}, st, gate);
   } else {
-    return launch_reduce<NQ, U>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
+    return launch_reduce<NQ, 1>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
   }
 }
 
 template <int NQ>
-static int spmv_fused_dispatch(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q,
+static int spmv_fused_dispatch(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q,
                                const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
                                SolveState* st = nullptr, int gate = GATE_NONE, int fin = FIN_NONE,
                                int fin_arg = 0) {
-  if (a->row64) {
-    if (a->max_row <= 4) return spmv_fused_t<NQ, int64_t, 4>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
-    return spmv_fused_t<NQ, int64_t, 8>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
-  }
-  if (a->max_row <= 4) return spmv_fused_t<NQ, int32_t, 4>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
-  return spmv_fused_t<NQ, int32_t, 8>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+  if (a->row64) return spmv_fused_t<NQ, int64_t>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+  return spmv_fused_t<NQ, int32_t>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
 }
 
-static int spmv_fused_any(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q, int nq,
+static int spmv_fused_any(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q, int nq,
                           const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
                           SolveState* st = nullptr, int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0) {
   switch (nq) {
@@ -340,57 +374,47 @@ static int spmv_fused_any(const pk_ctx* c, cudaStream_t s, const pk_mat* a, cons
   }
 }
 
-template <typename RowT, int W>
-static int residual_t(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* x, const double* b,
-                      double* r, double* copy1, double* copy2, double* part, SolveState* st, int gate, int fin,
-                      int fin_arg) {
-  OpResidual<RowT, W> op{csr_of<RowT>(a), x, b, r, copy1, copy2};
-  constexpr int U = W <= 4 ? 4 : 2;
-  return launch_reduce<1, U>(c, s, a->n_rows, op, ScalarPtrs{}, part, 1, 0, st, gate, nullptr, fin, fin_arg);
-}
-
-// r = b - A x (+ copies) with <r,r> partials.
-static int residual_any(const pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* x, const double* b,
+// r = b - A x (+ copies) with <r,r> partials (column col0 of a ld-wide array).
+static int residual_any(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* x, const double* b,
                         double* r, double* copy1, double* copy2, double* part, SolveState* st = nullptr,
-                        int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0) {
+                        int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0, int ld = 1, int col0 = 0) {
   if (a->row64) {
-    if (a->max_row <= 4) return residual_t<int64_t, 4>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg);
-    return residual_t<int64_t, 8>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg);
+    OpResidual<int64_t> op{csr_of<int64_t>(a), x, b, r, copy1, copy2};
+    return launch_reduce<1, 1>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
   }
-  if (a->max_row <= 4) return residual_t<int32_t, 4>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg);
-  return residual_t<int32_t, 8>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg);
+  OpResidual<int32_t> op{csr_of<int32_t>(a), x, b, r, copy1, copy2};
+  return launch_reduce<1, 1>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
 }
 
-static int dot_partials(const pk_ctx* c, cudaStream_t s, int64_t n, const double* x, const double* y,
+static int dot_partials(pk_ctx* c, cudaStream_t s, int64_t n, const double* x, const double* y,
                         double* part, SolveState* st = nullptr, int gate = GATE_NONE, int fin = FIN_NONE,
                         int fin_arg = 0) {
   OpDot op{x, y};
-  return launch_reduce<1, 8>(c, s, n, op, ScalarPtrs{}, part, 1, 0, st, gate, nullptr, fin, fin_arg);
+  return launch_reduce<1, 2>(c, s, n, op, ScalarPtrs{}, part, 1, 0, st, gate, nullptr, fin, fin_arg);
 }
 
 template <int NB>
-static int multidot_t(const pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* const* basis,
+static int multidot_t(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* const* basis,
                       const double* v, double* part, int ld, int col0, SolveState* st, int gate, int fin,
                       int fin_arg) {
   OpMultiDot<NB> op{};
   op.v = v;
   op.nb = nb;
   for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
-  constexpr int U = NB <= 2 ? 4 : (NB <= 8 ? 2 : 1);
-  return launch_reduce<NB, U>(c, s, n, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg, nb);
+  return launch_reduce<NB, 1>(c, s, n, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg, nb);
 }
 
-// Largest NB whose leaf stack fits in shared memory for this geometry.
+// Largest NB whose shared-memory footprint fits for this geometry.
 static int multidot_nb_cap(const pk_ctx* c, int64_t n) {
-  Geom geo = make_geom(n, c->ng, c->gs, 256);
+  Geom geo = make_geom(n, c->ng, c->gs);
   for (int nb : {32, 16, 8, 4, 2, 1}) {
-    if (engine_smem_bytes(geo, nb) <= 192 * 1024) return nb;
+    if (engine_smem_bytes(geo, nb, 1, false) <= 192 * 1024) return nb;
   }
   return 1;
 }
 
 // <b_j, v> partials for nb vectors, in passes of at most the smem cap.
-static int multidot_any(const pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* const* basis,
+static int multidot_any(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* const* basis,
                         const double* v, double* part, int ld, int col0, SolveState* st = nullptr,
                         int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0) {
   int cap = multidot_nb_cap(c, n);
@@ -413,18 +437,18 @@ static int multidot_any(const pk_ctx* c, cudaStream_t s, int64_t n, int nb, cons
 }
 
 template <int NB>
-static int gs_update_t(const pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
+static int gs_update_t(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
                        const double* coef_dev, double* part, SolveState* st, int gate, int fin, int fin_arg) {
   OpGsUpdate<NB> op{};
   op.v = v;
   op.nb = nb;
+  op.coef = coef_dev;
   for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
-  ScalarPtrs sp{coef_dev, nullptr, nullptr};
-  constexpr int U = NB <= 2 ? 4 : (NB <= 8 ? 2 : 1);
-  return launch_reduce<1, U>(c, s, n, op, sp, part, 1, 0, st, gate, nullptr, fin, fin_arg);
+  ScalarPtrs sp{coef_dev, nullptr, nullptr, nullptr};
+  return launch_reduce<1, 1>(c, s, n, op, sp, part, 1, 0, st, gate, nullptr, fin, fin_arg);
 }
 
-static int gs_update_any(const pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
+static int gs_update_any(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
                          const double* coef_dev, double* part, SolveState* st = nullptr, int gate = GATE_NONE,
                          int fin = FIN_NONE, int fin_arg = 0) {
   if (nb <= 1) return gs_update_t<1>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
@@ -472,6 +496,9 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (e == cudaSuccess) e = cudaMalloc(&c->scratch, sizeof(SolveState));
   if (e == cudaSuccess) e = cudaMalloc(&c->scratch_flag, 64 * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->scratch_d, 64 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&c->gtick, ((size_t)n_groups + 1) * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(c->gtick, 0, ((size_t)n_groups + 1) * sizeof(unsigned));
+  if (e == cudaSuccess) c->ticket = c->gtick + n_groups;
   if (e != cudaSuccess) {
     pk_ctx_destroy(c);
     return fail(PK_ERR_CUDA, std::string("context allocation: ") + cudaGetErrorString(e));
@@ -494,6 +521,8 @@ extern "C" int pk_ctx_destroy(pk_ctx* c) {
   if (c->scratch) cudaFree(c->scratch);
   if (c->scratch_flag) cudaFree(c->scratch_flag);
   if (c->scratch_d) cudaFree(c->scratch_d);
+  if (c->gtick) cudaFree(c->gtick);
+  if (c->spill) cudaFree(c->spill);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return PK_OK;
@@ -765,21 +794,23 @@ extern "C" int pk_spmv_fused(pk_ctx* c, const pk_mat* a, const double* p, double
       return fail(PK_ERR_INVALID, "result-with-input dot needs a square matrix");
     if (kinds[k] == PK_DOT_VECTOR && (!w || !w[k])) return fail(PK_ERR_INVALID, "missing fixed dot vector");
   }
+  PK_TRY(ensure_scratch(c, a->n_rows, nq));
   return spmv_fused_any(c, c->stream, a, p, q, nq, kinds, w, partials, nq, 0);
 }
 
 extern "C" int pk_reduce_stage1(pk_ctx* c, int64_t n, int32_t nq, const double* const* columns, double* partials) {
   PK_CHECK_CTX(c);
   if (!columns || !partials || n < 0) return fail(PK_ERR_INVALID, "bad argument");
+  PK_TRY(ensure_scratch(c, n, 4));
   // one launch per block of up to 4 columns (stacking never reorders, test_linalg.py:198-207)
   for (int q0 = 0; q0 < nq; q0 += 4) {
     int k = std::min(4, nq - q0);
     int rc;
     switch (k) {
-      case 1: { OpColumns<1> op{{columns[q0]}}; rc = launch_reduce<1, 8>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
-      case 2: { OpColumns<2> op{{columns[q0], columns[q0 + 1]}}; rc = launch_reduce<2, 4>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
-      case 3: { OpColumns<3> op{{columns[q0], columns[q0 + 1], columns[q0 + 2]}}; rc = launch_reduce<3, 4>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
-      default: { OpColumns<4> op{{columns[q0], columns[q0 + 1], columns[q0 + 2], columns[q0 + 3]}}; rc = launch_reduce<4, 2>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      case 1: { OpColumns<1> op{{columns[q0]}}; rc = launch_reduce<1, 2>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      case 2: { OpColumns<2> op{{columns[q0], columns[q0 + 1]}}; rc = launch_reduce<2, 2>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      case 3: { OpColumns<3> op{{columns[q0], columns[q0 + 1], columns[q0 + 2]}}; rc = launch_reduce<3, 1>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      default: { OpColumns<4> op{{columns[q0], columns[q0 + 1], columns[q0 + 2], columns[q0 + 3]}}; rc = launch_reduce<4, 1>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
     }
     PK_TRY(rc);
   }
@@ -798,6 +829,7 @@ extern "C" int pk_reduce_stage2(pk_ctx* c, int32_t nq, const double* partials, d
 extern "C" int pk_dot(pk_ctx* c, int64_t n, const double* x, const double* y, double* total) {
   PK_CHECK_CTX(c);
   if (!total || n < 0) return fail(PK_ERR_INVALID, "bad argument");
+  PK_TRY(ensure_scratch(c, n, 1));
   double* part = nullptr;
   PK_CUDA(cudaMallocAsync(&part, (size_t)c->ng * 8, c->stream));
   int rc = dot_partials(c, c->stream, n, x, y, part);
@@ -813,8 +845,9 @@ extern "C" int pk_cg_update(pk_ctx* c, int64_t n, double* x, double* r, double* 
                             double beta, double* partials) {
   PK_CHECK_CTX(c);
   if (!partials || n < 0) return fail(PK_ERR_INVALID, "bad argument");
+  PK_TRY(ensure_scratch(c, n, 1));
   OpCgUpdate op{x, r, p, ap, alpha, beta};
-  return launch_reduce<1, 8>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
+  return launch_reduce<1, 2>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
 }
 
 extern "C" int pk_bicg_s_update(pk_ctx* c, int64_t n, const double* r, const double* ap, const double* rr0p,
@@ -822,11 +855,12 @@ extern "C" int pk_bicg_s_update(pk_ctx* c, int64_t n, const double* r, const dou
                                 int32_t* breakdown) {
   PK_CHECK_CTX(c);
   if (!rr0p || !aprp || !partials || !alpha_out || !breakdown) return fail(PK_ERR_INVALID, "NULL argument");
+  PK_TRY(ensure_scratch(c, n, 1));
   k_bicg_alpha<<<1, 32, 0, c->stream>>>(rr0p, aprp, c->ng, btol, alpha_out, breakdown);
   PK_CUDA(cudaGetLastError());
   OpBicgS op{r, ap, s, 0.0};
   ScalarPtrs sp{alpha_out, nullptr, nullptr};
-  return launch_reduce<1, 8>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, breakdown);
+  return launch_reduce<1, 2>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, breakdown);
 }
 
 extern "C" int pk_bicg_xrp_update(pk_ctx* c, int64_t n, double* x, double* r, double* p, const double* s,
@@ -834,8 +868,9 @@ extern "C" int pk_bicg_xrp_update(pk_ctx* c, int64_t n, double* x, double* r, do
                                   const double* r0star, double* partials) {
   PK_CHECK_CTX(c);
   if (!partials || n < 0) return fail(PK_ERR_INVALID, "bad argument");
+  PK_TRY(ensure_scratch(c, n, 1));
   OpBicgXrp op{x, r, p, s, ap, as, r0star, alpha, omega, beta};
-  return launch_reduce<1, 4>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
+  return launch_reduce<1, 1>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
 }
 
 extern "C" int pk_gs_stage1(pk_ctx* c, int64_t n, int32_t nb, const double* const* basis, const double* v,
@@ -843,6 +878,7 @@ extern "C" int pk_gs_stage1(pk_ctx* c, int64_t n, int32_t nb, const double* cons
   PK_CHECK_CTX(c);
   if (nb < 0 || (nb > 0 && (!basis || !partials))) return fail(PK_ERR_INVALID, "bad argument");
   if (nb == 0) return PK_OK;
+  PK_TRY(ensure_scratch(c, n, std::min(nb, multidot_nb_cap(c, n))));
   return multidot_any(c, c->stream, n, nb, basis, v, partials, nb, 0);
 }
 
@@ -851,6 +887,7 @@ extern "C" int pk_gs_update(pk_ctx* c, int64_t n, double* v, int32_t nb, const d
   PK_CHECK_CTX(c);
   if (nb < 0 || !norm_partials || (nb > 0 && (!basis || !partials || !coeffs)))
     return fail(PK_ERR_INVALID, "bad argument");
+  PK_TRY(ensure_scratch(c, n, 1));
   if (nb > 0) {
     k_stage2<<<1, 32, 0, c->stream>>>(partials, c->ng, nb, nb, coeffs);
     PK_CUDA(cudaGetLastError());
@@ -863,11 +900,12 @@ extern "C" int pk_gs_normalize(pk_ctx* c, int64_t n, double* v, const double* no
   PK_CHECK_CTX(c);
   if (!norm_partials || !norm_out || !lucky || !partials) return fail(PK_ERR_INVALID, "NULL argument");
   double* inv = c->scratch_d;
+  PK_TRY(ensure_scratch(c, n, 1));
   k_norm_fin<<<1, 32, 0, c->stream>>>(norm_partials, c->ng, btol, norm_out, inv, lucky);
   PK_CUDA(cudaGetLastError());
   OpNormalize op{v, r, 0.0};
   ScalarPtrs sp{inv, nullptr, nullptr};
-  return launch_reduce<1, 8>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, lucky);
+  return launch_reduce<1, 2>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, lucky);
 }
 
 #include "pk_solvers.inc"

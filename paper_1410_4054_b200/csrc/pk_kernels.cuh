@@ -1,9 +1,10 @@
-// Fused kernels of the pipelined Krylov path (sm_100a).
+// Fused operators and finalizers of the pipelined Krylov path (sm_100a).
 //
-// Every reduction kernel is "elementwise op + ordered stage 1" (pk_reduce.cuh)
-// with an optional last-CTA finalizer that performs the serial stage 2 and the
-// host-side scalar recurrences of the reference on the device, so the next
-// kernel's prologue only reads a few scalars (SolveState).
+// Every reduction kernel is "per-row operator + ordered stage 1"
+// (pk_reduce.cuh) with an optional finalizer, run by the CTA that completes
+// the last group, which performs the serial stage 2 and the host-side scalar
+// recurrences of the reference on the device; the next kernel's prologue only
+// reads a few scalars (SolveState).
 //
 // Per-element arithmetic follows the reference exactly:
 //   SpMV row        acc = acc + v*x          _spmvkernels.py:12-18
@@ -12,6 +13,14 @@
 //   BiCG xrp        x+((a p)+(w s)); s-w As; ((p-w Ap) b)+r   fused.py:212-216
 //   GS update       v - sum_j (c_j b_j)      fused.py:268-272
 //   GS normalize    v * (1/||v||)            fused.py:300
+//
+// Recompute-at-gather fusion.  The solver-loop operators OpCgFused, OpBicgA
+// and OpBicgB fold a vector update into the SpMV that consumes it: the SpMV
+// input at a gathered column is recomputed from the old vectors with the very
+// same IEEE operations the update kernel would have used, so the result is
+// bit-identical to update-then-SpMV while the updated vector is never
+// re-read.  The updated vectors are written to the other half of a
+// ping-pong pair selected by SolveState::parity (flipped by the finalizer).
 #pragma once
 
 #include <math.h>
@@ -22,16 +31,17 @@
 namespace pk {
 
 // ---------------------------------------------------------------------------
-// finalizers (run by every thread of the last CTA of a launch)
+// finalizers (run by every thread of the finalizer CTA of a launch)
 // ---------------------------------------------------------------------------
 
 enum Fin : int32_t {
   FIN_NONE = 0,
-  FIN_CG_SETUP,
-  FIN_CG_ITER,
-  FIN_BICG_SETUP,
-  FIN_BICG_ALPHA,
-  FIN_BICG_TAIL,
+  FIN_CG_SETUP,    // p_rr, p_two, p_bb -> scale, alpha, beta
+  FIN_CG_FUSED,    // p_three [rr, pAp, ApAp] -> history, checks, alpha, beta; parity ^= 1
+  FIN_BICG_SETUP,  // p_pair col 0 (<r,r>), p_bb
+  FIN_BICG_ALPHA,  // p_pair [rr0, apr] -> alpha; arg: flip parity
+  FIN_BICG_TAIL,   // p_quad [ss, ass, asas, asr] -> omega, beta, history, checks
+  FIN_BICG_XTAIL,  // after the stand-alone xrp: parity ^= 1, STOPPED
   FIN_GM_RHO,      // cycle setup: rho (and scale on the first cycle)
   FIN_GM_NORM,     // ||w|| -> R diag, 1/||w|| or lucky
   FIN_GM_COEF,     // projections -> coef[], R column
@@ -42,76 +52,89 @@ enum Fin : int32_t {
 enum Gate : int32_t {
   GATE_NONE = 0,      // always run
   GATE_RUNNING = 1,   // run while status == RUNNING
-  GATE_TAIL = 2,      // run while status <= STOPPING (BiCGStab xrp)
+  GATE_STOPPING = 2,  // run only when status == STOPPING (BiCGStab tail update)
   GATE_GMRES = 3,     // run while status == RUNNING and not lucky
+  GATE_IN_GRAPH = 0x100,  // flag: the launch is a node of the WHILE graph body
+                          // (only such kernels may set the graph condition)
 };
 
-__device__ __forceinline__ void set_cond(SolveState* st, unsigned v) {
-  if (st->use_cond) cudaGraphSetConditional(st->cond, v);
+__device__ __forceinline__ void set_cond(SolveState* st, unsigned v, bool ing) {
+  if (ing && st->use_cond) cudaGraphSetConditional(st->cond, v);
 }
 
-__device__ __forceinline__ bool gate_open(SolveState* st, int gate) {
+__device__ __forceinline__ bool gate_open(SolveState* st, int gate, bool ing) {
   if (gate == GATE_NONE || st == nullptr) return true;
   int s = *(volatile int32_t*)&st->status;
   bool open;
-  if (gate == GATE_TAIL) open = s <= STOPPING;
+  if (gate == GATE_STOPPING) open = s == STOPPING;
   else if (gate == GATE_GMRES) open = (s == RUNNING) && !*(volatile int32_t*)&st->lucky;
   else open = (s == RUNNING);
-  if (!open && blockIdx.x == 0 && threadIdx.x == 0) set_cond(st, 0);
+  if (!open && gate != GATE_STOPPING && blockIdx.x == 0 && threadIdx.x == 0) set_cond(st, 0, ing);
   return open;
 }
 
 __device__ __forceinline__ double msqrt(double v) { return __dsqrt_rn(v); }
 
-__device__ inline void finalize(SolveState* st, int fin, int arg) {
+// CG scalar step (solvers.py:432-465): history, checks, alpha, beta.
+__device__ inline void cg_scalars(SolveState* st, double rr, double pap, double apap, bool setup, double bb, bool ing) {
+  st->rr = rr; st->pap = pap; st->apap = apap;
+  bool stop = false;
+  if (setup) {
+    double nb = msqrt(bb);
+    st->scale = nb > 0.0 ? nb : 1.0;
+    double entry = div_rn(msqrt(rr), st->scale);
+    if (entry <= st->tol && (!st->fixed || rr == 0.0)) {
+      st->term = PK_TERM_CONVERGED; stop = true;
+    } else if (fabs(pap) < st->btol_loop || pap == 0.0) {
+      st->term = PK_TERM_BREAKDOWN; st->kind = PK_BK_PAP; stop = true;
+    }
+  } else {
+    double mon = div_rn(msqrt(rr), st->scale);
+    st->hist[st->iter] = mon;
+    st->iter += 1;
+    if (!isfinite(mon)) {
+      st->term = PK_TERM_BREAKDOWN; st->kind = PK_BK_DIVERGENCE; stop = true;
+    } else if (mon <= st->tol && (!st->fixed || rr == 0.0)) {
+      st->term = PK_TERM_CONVERGED; stop = true;
+    } else if (fabs(pap) < st->btol_loop || pap == 0.0) {
+      st->term = PK_TERM_BREAKDOWN; st->kind = PK_BK_PAP; stop = true;
+    }
+  }
+  if (!stop) {
+    double a = div_rn(rr, pap);
+    st->alpha = a;
+    st->beta = sub_rn(div_rn(mul_rn(mul_rn(a, a), apap), rr), 1.0);
+    if (!setup && st->iter >= st->limit) { st->term = PK_TERM_MAX_ITER; stop = true; }
+  }
+  st->status = stop ? STOPPED : RUNNING;
+  set_cond(st, stop ? 0u : 1u, ing);
+}
+
+__device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
   const int th = threadIdx.x;
   const int ng = st->n_groups;
   __shared__ double tot[32];
   switch (fin) {
-    case FIN_CG_SETUP:
-    case FIN_CG_ITER: {
+    case FIN_CG_SETUP: {
       if (th == 0) tot[0] = stage2_col(st->p_rr, ng, 1, 0);
       if (th == 1) tot[1] = stage2_col(st->p_two, ng, 2, 0);
       if (th == 2) tot[2] = stage2_col(st->p_two, ng, 2, 1);
-      if (fin == FIN_CG_SETUP && th == 3) tot[3] = stage2_col(st->p_bb, ng, 1, 0);
+      if (th == 3) tot[3] = stage2_col(st->p_bb, ng, 1, 0);
       __syncthreads();
-      if (th != 0) return;
-      double rr = tot[0], pap = tot[1], apap = tot[2];
-      st->rr = rr; st->pap = pap; st->apap = apap;
-      bool stop = false;
-      if (fin == FIN_CG_SETUP) {
-        double nb = msqrt(tot[3]);
-        st->scale = nb > 0.0 ? nb : 1.0;
-        double entry = div_rn(msqrt(rr), st->scale);
-        if (entry <= st->tol && (!st->fixed || rr == 0.0)) {
-          st->term = PK_TERM_CONVERGED; stop = true;
-        } else if (fabs(pap) < st->btol_loop || pap == 0.0) {
-          st->term = PK_TERM_BREAKDOWN; st->kind = PK_BK_PAP; stop = true;
-        }
-      } else {
-        double mon = div_rn(msqrt(rr), st->scale);
-        st->hist[st->iter] = mon;
-        st->iter += 1;
-        if (!isfinite(mon)) {
-          st->term = PK_TERM_BREAKDOWN; st->kind = PK_BK_DIVERGENCE; stop = true;
-        } else if (mon <= st->tol && (!st->fixed || rr == 0.0)) {
-          st->term = PK_TERM_CONVERGED; stop = true;
-        } else if (fabs(pap) < st->btol_loop || pap == 0.0) {
-          st->term = PK_TERM_BREAKDOWN; st->kind = PK_BK_PAP; stop = true;
-        }
+      if (th == 0) cg_scalars(st, tot[0], tot[1], tot[2], true, tot[3], ing);
+      break;
+    }
+    case FIN_CG_FUSED: {
+      if (th < 3) tot[th] = stage2_col(st->p_three, ng, 3, th);
+      __syncthreads();
+      if (th == 0) {
+        st->parity ^= 1;
+        cg_scalars(st, tot[0], tot[1], tot[2], false, 0.0, ing);
       }
-      if (!stop) {
-        double a = div_rn(rr, pap);
-        st->alpha = a;
-        st->beta = sub_rn(div_rn(mul_rn(mul_rn(a, a), apap), rr), 1.0);
-        if (fin == FIN_CG_ITER && st->iter >= st->limit) { st->term = PK_TERM_MAX_ITER; stop = true; }
-      }
-      st->status = stop ? STOPPED : RUNNING;
-      set_cond(st, stop ? 0u : 1u);
       break;
     }
     case FIN_BICG_SETUP: {
-      if (th == 0) tot[0] = stage2_col(st->p_rr, ng, 1, 0);
+      if (th == 0) tot[0] = stage2_col(st->p_pair, ng, 2, 0);
       if (th == 1) tot[1] = stage2_col(st->p_bb, ng, 1, 0);
       __syncthreads();
       if (th != 0) return;
@@ -124,29 +147,30 @@ __device__ inline void finalize(SolveState* st, int fin, int arg) {
         st->term = PK_TERM_CONVERGED; stop = true;
       }
       st->status = stop ? STOPPED : RUNNING;
-      set_cond(st, stop ? 0u : 1u);
+      set_cond(st, stop ? 0u : 1u, ing);
       break;
     }
     case FIN_BICG_ALPHA: {
-      if (th == 0) tot[0] = stage2_col(st->p_rr, ng, 1, 0);
-      if (th == 1) tot[1] = stage2_col(st->p_apr, ng, 1, 0);
+      // fused_bicgstab_s_update's in-kernel alpha (fused.py:172-176)
+      if (th < 2) tot[th] = stage2_col(st->p_pair, ng, 2, th);
       __syncthreads();
       if (th != 0) return;
+      if (arg) st->parity ^= 1;
       double rho = tot[0], d = tot[1];
       st->rho0 = rho;
       st->apr = d;
       if (fabs(d) < st->btol_loop) {
         st->term = PK_TERM_BREAKDOWN; st->kind = PK_BK_APR0STAR;
         st->status = STOPPED;
-        set_cond(st, 0u);
+        set_cond(st, 0u, ing);
       } else {
         st->alpha = div_rn(rho, d);
       }
       break;
     }
     case FIN_BICG_TAIL: {
-      if (th == 0) tot[0] = stage2_col(st->p_ss, ng, 1, 0);
-      if (th >= 1 && th <= 3) tot[th] = stage2_col(st->p_tri, ng, 3, th - 1);
+      // solvers.py:647-684
+      if (th < 4) tot[th] = stage2_col(st->p_quad, ng, 4, th);
       __syncthreads();
       if (th != 0) return;
       double ss = tot[0], ass = tot[1], asas = tot[2], asr = tot[3], apr = st->apr;
@@ -186,7 +210,14 @@ __device__ inline void finalize(SolveState* st, int fin, int arg) {
         }
       }
       st->status = status;
-      set_cond(st, status == RUNNING ? 1u : 0u);
+      set_cond(st, status == RUNNING ? 1u : 0u, ing);
+      break;
+    }
+    case FIN_BICG_XTAIL: {
+      if (th == 0) {
+        st->parity ^= 1;
+        st->status = STOPPED;
+      }
       break;
     }
     case FIN_GM_RHO: {
@@ -242,122 +273,79 @@ __device__ inline void finalize(SolveState* st, int fin, int arg) {
 
 // Device scalar sources for an op: the solver points these at SolveState
 // fields written by the previous finalizer; kernel-level entries leave them
-// null and pass values.
+// null and pass values.  `par` selects the current half of ping-pong pairs.
 struct ScalarPtrs {
   const double* a;
   const double* b;
   const double* c;
+  const int32_t* par;
 };
 
 __device__ __forceinline__ double ld_scalar(const double* p, double v) { return p ? __ldcg(p) : v; }
+__device__ __forceinline__ int ld_par(const int32_t* p) { return p ? *(volatile const int32_t*)p : 0; }
 
 // ---------------------------------------------------------------------------
-// CSR row gather
+// SpMV operators (Op::kSpmv): the engine stages the CSR tile, the operator
+// supplies gload/gval (the SpMV input at a gathered column) and the per-row
+// epilogue.
 // ---------------------------------------------------------------------------
 
-template <typename RowT, int W>
-struct RowRegs {
-  RowT beg, end;
-  double v[W];
-  double xv[W];
-};
-
-template <typename RowT>
-struct Csr {
-  const RowT* rp;
-  const int32_t* ci;
-  const double* va;
-};
-
-template <typename RowT, int W>
-__device__ __forceinline__ void row_load(const Csr<RowT>& A, const double* __restrict__ x, int64_t row,
-                                         RowRegs<RowT, W>& it) {
-  it.beg = __ldg(A.rp + row);
-  it.end = __ldg(A.rp + row + 1);
-#pragma unroll
-  for (int s = 0; s < W; ++s) {
-    RowT e = it.beg + s;
-    if (e < it.end) {
-      int32_t c = __ldg(A.ci + e);
-      it.v[s] = __ldg(A.va + e);
-      it.xv[s] = __ldg(x + c);
-    }
-  }
-}
-
-template <typename RowT, int W>
-__device__ __forceinline__ double row_finish(const Csr<RowT>& A, const double* __restrict__ x,
-                                             const RowRegs<RowT, W>& it) {
-  double acc = 0.0;
-#pragma unroll
-  for (int s = 0; s < W; ++s) {
-    if (it.beg + s < it.end) acc = add_rn(acc, mul_rn(it.v[s], it.xv[s]));
-  }
-  for (RowT e = it.beg + W; e < it.end; ++e) acc = add_rn(acc, mul_rn(__ldg(A.va + e), __ldg(x + __ldg(A.ci + e))));
-  return acc;
-}
-
-// ---------------------------------------------------------------------------
-// elementwise operators
-// ---------------------------------------------------------------------------
-
-// q = A p with NQ fused dots (fused.py:86-120).
-template <typename RowT, int W, int NQ>
+// q = A p with NQ fused dots (fused.py:86-120); NQ = 0: plain spmv_csr.
+template <typename RowT, int NQ>
 struct OpSpmvFused {
+  static constexpr bool kSpmv = true;
+  static constexpr int kMinBlocks = 3;
+  static constexpr int kSlots = 8;
   Csr<RowT> A;
   const double* __restrict__ p;
-  double* __restrict__ q;
+  double* q;
   int32_t kind[4];
   const double* w[4];
   struct Item {
-    RowRegs<RowT, W> r;
     double pv;
     double wv[NQ > 0 ? NQ : 1];
   };
   __device__ __forceinline__ void load(int64_t row, Item& it) const {
-    row_load<RowT, W>(A, p, row, it.r);
-    bool need_p = false;
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
-      if (kind[k] == PK_DOT_INPUT) need_p = true;
+      if (kind[k] == PK_DOT_INPUT) it.pv = __ldg(p + row);
       if (kind[k] == PK_DOT_VECTOR) it.wv[k] = __ldg(w[k] + row);
     }
-    if (need_p) it.pv = __ldg(p + row);
   }
-  __device__ __forceinline__ void compute(int64_t row, Item& it, double (&c)[NQ > 0 ? NQ : 1]) const {
-    double acc = row_finish<RowT, W>(A, p, it.r);
+  struct Gat { double v; };
+  __device__ __forceinline__ void gload(int32_t col, Gat& g) const { g.v = __ldg(p + col); }
+  __device__ __forceinline__ double gval(const Gat& g) const { return g.v; }
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t row, Item& it, double acc, double (&c)[M]) const {
     if (q) q[row] = acc;
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) {
+    for (int k = 0; k < NQ && k < M; ++k) {
       c[k] = kind[k] == PK_DOT_INPUT ? mul_rn(acc, it.pv)
            : kind[k] == PK_DOT_RESULT ? mul_rn(acc, acc) : mul_rn(acc, it.wv[k]);
     }
-  }
-  __device__ __forceinline__ void apply(int64_t row, Item& it) const {
-    q[row] = row_finish<RowT, W>(A, p, it.r);
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs&) {}
 };
 
 // r = b + (-1) A x (add_scaled, linalg.py:450-457); optional copies; <r,r>.
-template <typename RowT, int W>
+template <typename RowT>
 struct OpResidual {
+  static constexpr bool kSpmv = true;
+  static constexpr int kMinBlocks = 3;
+  static constexpr int kSlots = 8;
   Csr<RowT> A;
   const double* __restrict__ x;
   const double* __restrict__ b;
   double* r;
   double* copy1;
   double* copy2;
-  struct Item {
-    RowRegs<RowT, W> r;
-    double bv;
-  };
-  __device__ __forceinline__ void load(int64_t row, Item& it) const {
-    row_load<RowT, W>(A, x, row, it.r);
-    it.bv = __ldg(b + row);
-  }
-  __device__ __forceinline__ void compute(int64_t row, Item& it, double (&c)[1]) const {
-    double q = row_finish<RowT, W>(A, x, it.r);
+  struct Item { double bv; };
+  __device__ __forceinline__ void load(int64_t row, Item& it) const { it.bv = __ldg(b + row); }
+  struct Gat { double v; };
+  __device__ __forceinline__ void gload(int32_t col, Gat& g) const { g.v = __ldg(x + col); }
+  __device__ __forceinline__ double gval(const Gat& g) const { return g.v; }
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t row, Item& it, double q, double (&c)[M]) const {
     double rv = add_rn(it.bv, mul_rn(-1.0, q));
     if (r) r[row] = rv;
     if (copy1) copy1[row] = rv;
@@ -367,9 +355,198 @@ struct OpResidual {
   __device__ __forceinline__ void scalars(const ScalarPtrs&) {}
 };
 
+// One pipelined-CG iteration in one kernel (fused.py:123-151 + 86-120):
+//   r' = r - a Ap;  p' = p b + r';  x += a p;  Ap' = A p';
+//   contributions [r'.r', Ap'.p', Ap'.Ap'].
+// p' at a gathered column is recomputed from (p, r, Ap) there.
+template <typename RowT>
+struct OpCgFused {
+  static constexpr bool kSpmv = true;
+  static constexpr int kMinBlocks = 2;
+  static constexpr int kSlots = 4;
+  Csr<RowT> A;
+  double* x;
+  double* r[2];
+  double* p[2];
+  double* ap[2];
+  double alpha, beta;
+  const double* rc;  // current halves, resolved in scalars()
+  const double* pc;
+  const double* apc;
+  double* rn_;
+  double* pn_;
+  double* apn_;
+  struct Item { double x, r, p, ap; };
+  __device__ __forceinline__ void load(int64_t row, Item& it) const {
+    it.x = x[row]; it.r = rc[row]; it.p = pc[row]; it.ap = apc[row];
+  }
+  struct Gat { double r, ap, p; };
+  __device__ __forceinline__ void gload(int32_t col, Gat& g) const {
+    g.r = __ldg(rc + col); g.ap = __ldg(apc + col); g.p = __ldg(pc + col);
+  }
+  __device__ __forceinline__ double gval(const Gat& g) const {
+    double rn = sub_rn(g.r, mul_rn(alpha, g.ap));
+    return add_rn(mul_rn(g.p, beta), rn);
+  }
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t row, Item& it, double q, double (&c)[M]) const {
+    double xn = add_rn(it.x, mul_rn(alpha, it.p));
+    double rn = sub_rn(it.r, mul_rn(alpha, it.ap));
+    double pn = add_rn(mul_rn(it.p, beta), rn);
+    x[row] = xn; rn_[row] = rn; pn_[row] = pn; apn_[row] = q;
+    c[0] = mul_rn(rn, rn);
+    c[1] = mul_rn(q, pn);
+    c[2] = mul_rn(q, q);
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    alpha = ld_scalar(sp.a, alpha);
+    beta = ld_scalar(sp.b, beta);
+    const int cur = ld_par(sp.par);
+    rc = cur ? r[1] : r[0]; pc = cur ? p[1] : p[0]; apc = cur ? ap[1] : ap[0];
+    rn_ = cur ? r[0] : r[1]; pn_ = cur ? p[0] : p[1]; apn_ = cur ? ap[0] : ap[1];
+  }
+};
+
+// BiCGStab second SpMV with the s-update folded in (fused.py:154-182 + 86-120):
+//   s = r - a Ap (recomputed at every gathered column, never stored);
+//   As = A s;  contributions [s.s, As.s, As.As, As.r0*].
+template <typename RowT>
+struct OpBicgB {
+  static constexpr bool kSpmv = true;
+  static constexpr int kMinBlocks = 2;
+  static constexpr int kSlots = 6;
+  Csr<RowT> A;
+  const double* r[2];
+  const double* ap[2];
+  const double* __restrict__ r0;
+  double* as;
+  double alpha;
+  const double* rc;
+  const double* apc;
+  struct Item { double s, r0; };
+  __device__ __forceinline__ void load(int64_t row, Item& it) const {
+    it.s = sub_rn(__ldg(rc + row), mul_rn(alpha, __ldg(apc + row)));
+    it.r0 = __ldg(r0 + row);
+  }
+  struct Gat { double r, ap; };
+  __device__ __forceinline__ void gload(int32_t col, Gat& g) const { g.r = __ldg(rc + col); g.ap = __ldg(apc + col); }
+  __device__ __forceinline__ double gval(const Gat& g) const { return sub_rn(g.r, mul_rn(alpha, g.ap)); }
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t row, Item& it, double q, double (&c)[M]) const {
+    as[row] = q;
+    c[0] = mul_rn(it.s, it.s);
+    c[1] = mul_rn(q, it.s);
+    c[2] = mul_rn(q, q);
+    c[3] = mul_rn(q, it.r0);
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    alpha = ld_scalar(sp.a, alpha);
+    const int cur = ld_par(sp.par);
+    rc = cur ? r[1] : r[0];
+    apc = cur ? ap[1] : ap[0];
+  }
+};
+
+// BiCGStab xrp update of iteration k fused with the first SpMV of k+1
+// (fused.py:185-219 + 86-120):
+//   s = r - a Ap;  x += (a p) + (w s);  r' = s - w As;  p' = ((p - w Ap) b) + r';
+//   Ap' = A p';  contributions [r'.r0*, Ap'.r0*].
+template <typename RowT>
+struct OpBicgA {
+  static constexpr bool kSpmv = true;
+  static constexpr int kMinBlocks = 2;
+  static constexpr int kSlots = 4;
+  Csr<RowT> A;
+  double* x;
+  double* r[2];
+  double* p[2];
+  double* ap[2];
+  const double* __restrict__ as;
+  const double* __restrict__ r0;
+  double alpha, omega, beta;
+  const double* rc;
+  const double* pc;
+  const double* apc;
+  double* rn_;
+  double* pn_;
+  double* apn_;
+  struct Item { double x, r, p, ap, as, r0; };
+  __device__ __forceinline__ void load(int64_t row, Item& it) const {
+    it.x = x[row]; it.r = rc[row]; it.p = pc[row]; it.ap = apc[row];
+    it.as = __ldg(as + row); it.r0 = __ldg(r0 + row);
+  }
+  struct Gat { double r, ap, as, p; };
+  __device__ __forceinline__ void gload(int32_t col, Gat& g) const {
+    g.r = __ldg(rc + col); g.ap = __ldg(apc + col); g.as = __ldg(as + col); g.p = __ldg(pc + col);
+  }
+  __device__ __forceinline__ double gval(const Gat& g) const {
+    double s = sub_rn(g.r, mul_rn(alpha, g.ap));
+    double rn = sub_rn(s, mul_rn(omega, g.as));
+    return add_rn(mul_rn(sub_rn(g.p, mul_rn(omega, g.ap)), beta), rn);
+  }
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t row, Item& it, double q, double (&c)[M]) const {
+    double s = sub_rn(it.r, mul_rn(alpha, it.ap));
+    double xn = add_rn(it.x, add_rn(mul_rn(alpha, it.p), mul_rn(omega, s)));
+    double rn = sub_rn(s, mul_rn(omega, it.as));
+    double pn = add_rn(mul_rn(sub_rn(it.p, mul_rn(omega, it.ap)), beta), rn);
+    x[row] = xn; rn_[row] = rn; pn_[row] = pn; apn_[row] = q;
+    c[0] = mul_rn(rn, it.r0);
+    c[1] = mul_rn(q, it.r0);
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    alpha = ld_scalar(sp.a, alpha);
+    omega = ld_scalar(sp.b, omega);
+    beta = ld_scalar(sp.c, beta);
+    const int cur = ld_par(sp.par);
+    rc = cur ? r[1] : r[0]; pc = cur ? p[1] : p[0]; apc = cur ? ap[1] : ap[0];
+    rn_ = cur ? r[0] : r[1]; pn_ = cur ? p[0] : p[1]; apn_ = cur ? ap[0] : ap[1];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// elementwise operators
+// ---------------------------------------------------------------------------
+
+// Stand-alone BiCGStab xrp of the final iteration (s recomputed from r, Ap);
+// contribution r'.r0* (the rr0 partials a resumed loop needs).
+struct OpBicgXrpTail {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
+  double* x;
+  double* r[2];
+  double* p[2];
+  const double* ap[2];
+  const double* __restrict__ as;
+  const double* __restrict__ r0;
+  double alpha, omega, beta;
+  int cur;
+  struct Item { double x, r, p, ap, as, r0; };
+  __device__ __forceinline__ void load(int64_t i, Item& it) const {
+    it.x = x[i]; it.r = (cur ? r[1] : r[0])[i]; it.p = (cur ? p[1] : p[0])[i]; it.ap = __ldg((cur ? ap[1] : ap[0]) + i);
+    it.as = __ldg(as + i); it.r0 = __ldg(r0 + i);
+  }
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
+    double s = sub_rn(it.r, mul_rn(alpha, it.ap));
+    double xn = add_rn(it.x, add_rn(mul_rn(alpha, it.p), mul_rn(omega, s)));
+    double rn = sub_rn(s, mul_rn(omega, it.as));
+    double pn = add_rn(mul_rn(sub_rn(it.p, mul_rn(omega, it.ap)), beta), rn);
+    x[i] = xn; (cur ? r[0] : r[1])[i] = rn; (cur ? p[0] : p[1])[i] = pn;
+    c[0] = mul_rn(rn, it.r0);
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    alpha = ld_scalar(sp.a, alpha);
+    omega = ld_scalar(sp.b, omega);
+    beta = ld_scalar(sp.c, beta);
+    cur = ld_par(sp.par);
+  }
+};
 
 // fused_cg_vector_update (fused.py:123-151)
 struct OpCgUpdate {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
   double* x;
   double* r;
   double* p;
@@ -379,7 +556,8 @@ struct OpCgUpdate {
   __device__ __forceinline__ void load(int64_t i, Item& it) const {
     it.x = x[i]; it.r = r[i]; it.p = p[i]; it.ap = __ldg(ap + i);
   }
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[1]) const {
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
     double xn = add_rn(it.x, mul_rn(alpha, it.p));
     double rn = sub_rn(it.r, mul_rn(alpha, it.ap));
     double pn = add_rn(mul_rn(it.p, beta), rn);
@@ -394,13 +572,16 @@ struct OpCgUpdate {
 
 // fused_bicgstab_s_update (fused.py:154-182): s = r - alpha Ap, <s,s>
 struct OpBicgS {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
   const double* __restrict__ r;
   const double* __restrict__ ap;
   double* s;
   double alpha;
   struct Item { double r, ap; };
   __device__ __forceinline__ void load(int64_t i, Item& it) const { it.r = __ldg(r + i); it.ap = __ldg(ap + i); }
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[1]) const {
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
     double sv = sub_rn(it.r, mul_rn(alpha, it.ap));
     s[i] = sv;
     c[0] = mul_rn(sv, sv);
@@ -410,6 +591,8 @@ struct OpBicgS {
 
 // fused_bicgstab_xrp_update (fused.py:185-219)
 struct OpBicgXrp {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
   double* x;
   double* r;
   double* p;
@@ -422,7 +605,8 @@ struct OpBicgXrp {
   __device__ __forceinline__ void load(int64_t i, Item& it) const {
     it.x = x[i]; it.p = p[i]; it.s = __ldg(s + i); it.ap = __ldg(ap + i); it.as = __ldg(as + i); it.r0 = __ldg(r0 + i);
   }
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[1]) const {
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
     double xn = add_rn(it.x, add_rn(mul_rn(alpha, it.p), mul_rn(omega, it.s)));
     double rn = sub_rn(it.s, mul_rn(omega, it.as));
     double pn = add_rn(mul_rn(sub_rn(it.p, mul_rn(omega, it.ap)), beta), rn);
@@ -438,26 +622,32 @@ struct OpBicgXrp {
 
 // x * y contributions (dot, reduce_stage1 of a product)
 struct OpDot {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
   const double* __restrict__ x;
   const double* __restrict__ y;
   struct Item { double x, y; };
   __device__ __forceinline__ void load(int64_t i, Item& it) const { it.x = __ldg(x + i); it.y = __ldg(y + i); }
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[1]) const { c[0] = mul_rn(it.x, it.y); }
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const { c[0] = mul_rn(it.x, it.y); }
   __device__ __forceinline__ void scalars(const ScalarPtrs&) {}
 };
 
 // NQ precomputed contribution columns (reduce_stage1 of stacked streams).
 template <int NQ>
 struct OpColumns {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
   const double* col[NQ];
   struct Item { double v[NQ]; };
   __device__ __forceinline__ void load(int64_t i, Item& it) const {
 #pragma unroll
     for (int k = 0; k < NQ; ++k) it.v[k] = __ldg(col[k] + i);
   }
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[NQ]) const {
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) c[k] = it.v[k];
+    for (int k = 0; k < NQ && k < M; ++k) c[k] = it.v[k];
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs&) {}
 };
@@ -465,6 +655,8 @@ struct OpColumns {
 // fused_gs_stage1 (fused.py:222-243): <b_j, v> for j < nb (nb <= NB).
 template <int NB>
 struct OpMultiDot {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
   const double* __restrict__ v;
   int32_t nb;
   const double* b[NB];
@@ -474,9 +666,10 @@ struct OpMultiDot {
 #pragma unroll
     for (int j = 0; j < NB; ++j) if (j < nb) it.b[j] = __ldg(b[j] + i);
   }
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[NB]) const {
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
 #pragma unroll
-    for (int j = 0; j < NB; ++j) c[j] = j < nb ? mul_rn(it.b[j], it.v) : 0.0;
+    for (int j = 0; j < NB && j < M; ++j) c[j] = j < nb ? mul_rn(it.b[j], it.v) : 0.0;
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs&) {}
 };
@@ -484,40 +677,43 @@ struct OpMultiDot {
 // fused_gs_update (fused.py:246-277): v -= sum_j c_j b_j; <v,v>.
 template <int NB>
 struct OpGsUpdate {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = NB > 8 ? 2 : 4;
   double* v;
   int32_t nb;
   const double* b[NB];
-  double c[NB];
+  const double* coef;  // device [nb], finalized by the previous kernel
   struct Item { double v; double b[NB]; };
   __device__ __forceinline__ void load(int64_t i, Item& it) const {
     it.v = v[i];
 #pragma unroll
     for (int j = 0; j < NB; ++j) if (j < nb) it.b[j] = __ldg(b[j] + i);
   }
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&cc)[1]) const {
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&cc)[M]) const {
     double acc = 0.0;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(c[j], it.b[j]));
+    for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(__ldg(coef + j), it.b[j]));
     double vn = nb > 0 ? sub_rn(it.v, acc) : it.v;
     v[i] = vn;
     cc[0] = mul_rn(vn, vn);
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
-    if (sp.a) {
-#pragma unroll
-      for (int j = 0; j < NB; ++j) c[j] = j < nb ? __ldcg(sp.a + j) : 0.0;
-    }
+    if (sp.a) coef = sp.a;
   }
 };
 
 // fused_gs_normalize (fused.py:280-305): v *= inv; <r, v>.
 struct OpNormalize {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
   double* v;
   const double* __restrict__ r;
   double inv;
   struct Item { double v, r; };
   __device__ __forceinline__ void load(int64_t i, Item& it) const { it.v = v[i]; it.r = __ldg(r + i); }
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[1]) const {
+  template <int M>
+  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
     double vn = mul_rn(it.v, inv);
     v[i] = vn;
     c[0] = mul_rn(it.r, vn);

@@ -33,6 +33,8 @@ struct SolveState {
   int32_t half_step;  // BiCGStab: converged on the half step
   int32_t lucky;      // GMRES: lucky breakdown inside the cycle
   int32_t step;       // GMRES: completed steps in the current cycle
+  int32_t parity;     // current half of the ping-pong vector pairs
+  int32_t pad3;
 
   // scalars
   double scale;       // ||b|| or 1
@@ -54,6 +56,9 @@ struct SolveState {
   double* p_ss;       // [ng]       BiCG <s,s>
   double* p_tri;      // [ng x 3]   BiCG {As.s, As.As, As.r0*}
   double* p_ww;       // [ng]       GMRES <w,w>
+  double* p_three;    // [ng x 3]   fused CG {rr, pAp, ApAp}
+  double* p_pair;     // [ng x 2]   BiCG {<r,r0*>, <Ap,r0*>}
+  double* p_quad;     // [ng x 4]   BiCG {ss, As.s, As.As, As.r0*}
   double* p_coef;     // [ng x m]   GMRES projections (older basis + newest)
   double* p_xi;       // [m x ng]   GMRES <r, v_i> per step
   double* coef;       // [m]        finalized projection coefficients

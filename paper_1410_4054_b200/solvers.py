@@ -190,7 +190,7 @@ def _native_config(cfg: SolverConfig) -> N.PkConfig:
         tolerance=cfg.tolerance, max_iterations=cfg.max_iterations, restart=cfg.restart,
         breakdown_tolerance=cfg.breakdown_tolerance,
         fixed_iterations=cfg.fixed_iterations if cfg.fixed else 0,
-        loop_mode=N.LOOP_GRAPH if cfg.loop_mode == "graph" else N.LOOP_HOST, reserved=0)
+        loop_mode=N.LOOP_GRAPH if cfg.loop_mode == "graph" else N.LOOP_HOST, flags=0)
 
 
 def _trace_from(res: N.PkResult, method: str, n: int, restart: int) -> ExecutionTrace:
@@ -252,13 +252,16 @@ def _run(method: str, a, b, x0, config, context, debug):
 
 
 def cg_pipelined(a, b, x0=None, config=None, context=None, debug=False) -> SolverResult:
-    """Pipelined CG (solvers.py:395-469): 2 fused kernels per iteration, the
-    stage-2 reduction and alpha/beta/convergence finalized on the device."""
+    """Pipelined CG (solvers.py:395-469): ONE fused kernel per iteration (the
+    vector update folded into the SpMV by recompute-at-gather), the stage-2
+    reduction and alpha/beta/convergence finalized on the device."""
     return _run("cg", a, b, x0, config, context, debug)
 
 
 def bicgstab_pipelined(a, b, x0=None, config=None, context=None, debug=False) -> SolverResult:
-    """Pipelined BiCGStab (solvers.py:583-712): 4 fused kernels per iteration."""
+    """Pipelined BiCGStab (solvers.py:583-712): 2 fused kernels per iteration
+    (the reference's 4; s-update folded into the As-SpMV, xrp update into the
+    next iteration's Ap-SpMV)."""
     return _run("bicgstab", a, b, x0, config, context, debug)
 
 
@@ -287,11 +290,15 @@ def solve(A, b, tag=("cg", "pipelined"), tol: float = 1e-8, maxiter: int = 500, 
     return SOLVERS[tuple(tag)](A, b, x0=x0, config=cfg, context=context)
 
 
-def solve_resident(method: str, a, b, x0=None, config=None, context=None):
+def solve_resident(method: str, a, b, x0=None, config=None, context=None, profile: bool = False):
     """HBM-resident solve: ``a`` a DeviceMatrix (or CsrMatrix, uploaded once),
     ``b``/``x0`` float64 CUDA tensors; returns (x tensor, SolverResult without
     a host copy of x).  No host<->device vector traffic besides the history --
-    the entry the benchmark times (pk_solve_device)."""
+    the entry the benchmark times (pk_solve_device).
+
+    ``profile=True`` (needs ``loop_mode="host"``) brackets every loop kernel
+    with CUDA events; the per-kernel times land in
+    ``diagnostics["kernel_seconds"]`` / ``["kernel_launches"]``."""
     import torch
 
     cfg = SolverConfig.coerce(config)
@@ -308,6 +315,10 @@ def solve_resident(method: str, a, b, x0=None, config=None, context=None):
     hist = np.empty(max(cfg.iteration_limit(), 1))
     res = N.PkResult()
     ncfg = _native_config(cfg)
+    if profile:
+        if cfg.loop_mode != "host":
+            raise ValueError("kernel profiling needs loop_mode='host'")
+        ncfg.flags = N.FLAG_PROFILE
     x0p = None
     if x0 is not None:
         x0 = x0.contiguous()
@@ -322,5 +333,7 @@ def solve_resident(method: str, a, b, x0=None, config=None, context=None):
         true_final_residual=float(res.true_final_residual), iterations=int(res.iterations),
         termination=N.TERM_NAMES[res.termination], trace=_trace_from(res, method, n, cfg.restart),
         breakdown_kind=N.KIND_NAMES[res.breakdown_kind], loop_seconds=float(res.loop_seconds),
-        diagnostics={"launches": res.total_launches, "launches_per_iteration": res.launches_per_iteration})
+        diagnostics={"launches": res.total_launches, "launches_per_iteration": res.launches_per_iteration,
+                     "kernel_seconds": [float(v) for v in res.kernel_seconds],
+                     "kernel_launches": [int(v) for v in res.kernel_launches]})
     return x, result
