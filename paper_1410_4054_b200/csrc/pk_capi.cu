@@ -10,8 +10,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "pipekrylov_b200.h"
@@ -97,15 +99,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
   Op op = op0;
   op.scalars(sp);
   bool last = engine_run<NQ, U>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
-  if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing);
+  if (last && fin != FIN_NONE && st && threadIdx.x < 32) finalize(st, fin, fin_arg, ing);  // warp 0 of the last CTA
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kThreads, 3) k_sweep(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
-  extern __shared__ double smem[];
+__global__ void __launch_bounds__(256, 4) k_sweep(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
   if (st && !gate_open(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0)) return;
   op.scalars(sp);
-  sweep_tiles(n, op, smem);
+  sweep_rows(n, op);
 }
 
 __global__ void k_finalize(SolveState* st, int fin, int arg) { finalize(st, fin, arg, false); }
@@ -279,9 +280,9 @@ static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
 static Scratch scratch_of(const pk_ctx* c) { return Scratch{c->spill, c->gtick, c->ticket}; }
 
 template <class K>
-static int engine_grid(const pk_ctx* c, K kern, size_t smem, int64_t units) {
+static int engine_grid(const pk_ctx* c, K kern, size_t smem, int64_t units, int threads = kThreads) {
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
   int64_t cap = (int64_t)c->sm_count * occ;
   return (int)std::max<int64_t>(1, std::min<int64_t>(units, cap));
 }
@@ -292,7 +293,13 @@ static int grid_elem(const pk_ctx* c, int64_t n, int block) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
 }
 
-template <int NQ, int U, class Op>
+// U = rows per thread per batch (chunks per batch = 8 U).
+template <class Op, class = void>
+struct RowsPerThread { static constexpr int value = 2; };
+template <class Op>
+struct RowsPerThread<Op, std::void_t<decltype(Op::kRowsPerThread)>> { static constexpr int value = Op::kRowsPerThread; };
+
+template <int NQ, class Op, int U = (NQ <= 4 ? RowsPerThread<Op>::value : 1)>
 static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp,
                          double* part, int ld, int col0, SolveState* st = nullptr, int gate = GATE_NONE,
                          const int32_t* skip = nullptr, int fin = FIN_NONE, int fin_arg = 0,
@@ -300,7 +307,7 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
   Geom geo = make_geom(n, c->ng, c->gs);
   if (!geo.leaf && (size_t)geo.G * (size_t)nstore > c->spill_cap)
     return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
-  size_t smem = engine_smem_bytes(geo, NQ, U, Op::kSpmv);
+  size_t smem = engine_smem_bytes(geo, NQ, U);
   constexpr int MINB = NQ > 8 ? 1 : (NQ > 4 ? 2 : Op::kMinBlocks);
   auto kern = k_reduce<NQ, U, MINB, Op>;
   if (smem + 1024 > 48 * 1024) {
@@ -321,10 +328,8 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
 template <class Op>
 static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp = ScalarPtrs{},
                         SolveState* st = nullptr, int gate = GATE_NONE) {
-  size_t smem = Op::kSpmv ? (size_t)kWarps * kPCap * sizeof(double) : 0;
   auto kern = k_sweep<Op>;
-  int64_t tiles = (n + 31) / 32;
-  kern<<<engine_grid(c, kern, smem, (tiles + kWarps - 1) / kWarps), kThreads, smem, s>>>(n, op, sp, st, gate);
+  kern<<<engine_grid(c, kern, 0, (n + 255) / 256, 256), 256, 0, s>>>(n, op, sp, st, gate);
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
@@ -334,12 +339,16 @@ static Csr<RowT> csr_of(const pk_mat* a) {
   return Csr<RowT>{(const RowT*)a->rowptr, a->cols, a->vals};
 }
 
-// SpMV with NQ fused dots; dispatch on the row index type.
-template <int NQ, typename RowT>
+// nnz slots per lane per pass of the SpMV tile loop: 5 (2-D 5-point rows) or
+// 7 (3-D 7-point and anything longer; longer rows take several passes).
+static inline bool wide_rows(const pk_mat* a) { return a->max_row > 5; }
+
+// SpMV with NQ fused dots; dispatch on the row index type and slot count.
+template <int NQ, typename RowT, int S>
 static int spmv_fused_t(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q,
                         const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
                         SolveState* st, int gate, int fin, int fin_arg) {
-  OpSpmvFused<RowT, NQ> op{};
+  OpSpmvFused<RowT, NQ, S> op{};
   op.A = csr_of<RowT>(a);
   op.p = p;
   op.q = q;
@@ -348,7 +357,7 @@ static int spmv_fused_t(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double
   if constexpr (NQ == 0) {
     return launch_sweep(c, s, a->n_rows, op, ScalarPtrs{}, st, gate);
   } else {
-    return launch_reduce<NQ, 1>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
+    return launch_reduce<NQ>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
   }
 }
 
@@ -357,8 +366,12 @@ static int spmv_fused_dispatch(pk_ctx* c, cudaStream_t s, const pk_mat* a, const
                                const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
                                SolveState* st = nullptr, int gate = GATE_NONE, int fin = FIN_NONE,
                                int fin_arg = 0) {
-  if (a->row64) return spmv_fused_t<NQ, int64_t>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
-  return spmv_fused_t<NQ, int32_t>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+  if (a->row64) {
+    if (wide_rows(a)) return spmv_fused_t<NQ, int64_t, 7>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+    return spmv_fused_t<NQ, int64_t, 5>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+  }
+  if (wide_rows(a)) return spmv_fused_t<NQ, int32_t, 7>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+  return spmv_fused_t<NQ, int32_t, 5>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
 }
 
 static int spmv_fused_any(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q, int nq,
@@ -374,23 +387,37 @@ static int spmv_fused_any(pk_ctx* c, cudaStream_t s, const pk_mat* a, const doub
   }
 }
 
+template <typename RowT, int S>
+static int residual_t(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* x, const double* b, double* r,
+                      double* copy1, double* copy2, double* part, SolveState* st, int gate, int fin, int fin_arg,
+                      int ld, int col0) {
+  OpResidual<RowT, S> op{};
+  op.A = csr_of<RowT>(a);
+  op.x = x;
+  op.b = b;
+  op.r = r;
+  op.copy1 = copy1;
+  op.copy2 = copy2;
+  return launch_reduce<1>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
+}
+
 // r = b - A x (+ copies) with <r,r> partials (column col0 of a ld-wide array).
 static int residual_any(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* x, const double* b,
                         double* r, double* copy1, double* copy2, double* part, SolveState* st = nullptr,
                         int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0, int ld = 1, int col0 = 0) {
   if (a->row64) {
-    OpResidual<int64_t> op{csr_of<int64_t>(a), x, b, r, copy1, copy2};
-    return launch_reduce<1, 1>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
+    if (wide_rows(a)) return residual_t<int64_t, 7>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
+    return residual_t<int64_t, 5>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
   }
-  OpResidual<int32_t> op{csr_of<int32_t>(a), x, b, r, copy1, copy2};
-  return launch_reduce<1, 1>(c, s, a->n_rows, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg);
+  if (wide_rows(a)) return residual_t<int32_t, 7>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
+  return residual_t<int32_t, 5>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
 }
 
 static int dot_partials(pk_ctx* c, cudaStream_t s, int64_t n, const double* x, const double* y,
                         double* part, SolveState* st = nullptr, int gate = GATE_NONE, int fin = FIN_NONE,
                         int fin_arg = 0) {
   OpDot op{x, y};
-  return launch_reduce<1, 2>(c, s, n, op, ScalarPtrs{}, part, 1, 0, st, gate, nullptr, fin, fin_arg);
+  return launch_reduce<1>(c, s, n, op, ScalarPtrs{}, part, 1, 0, st, gate, nullptr, fin, fin_arg);
 }
 
 template <int NB>
@@ -401,14 +428,14 @@ static int multidot_t(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double
   op.v = v;
   op.nb = nb;
   for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
-  return launch_reduce<NB, 1>(c, s, n, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg, nb);
+  return launch_reduce<NB>(c, s, n, op, ScalarPtrs{}, part, ld, col0, st, gate, nullptr, fin, fin_arg, nb);
 }
 
 // Largest NB whose shared-memory footprint fits for this geometry.
 static int multidot_nb_cap(const pk_ctx* c, int64_t n) {
   Geom geo = make_geom(n, c->ng, c->gs);
   for (int nb : {32, 16, 8, 4, 2, 1}) {
-    if (engine_smem_bytes(geo, nb, 1, false) <= 192 * 1024) return nb;
+    if (engine_smem_bytes(geo, nb, 1) <= 192 * 1024) return nb;
   }
   return 1;
 }
@@ -445,7 +472,7 @@ static int gs_update_t(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, 
   op.coef = coef_dev;
   for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
   ScalarPtrs sp{coef_dev, nullptr, nullptr, nullptr};
-  return launch_reduce<1, 1>(c, s, n, op, sp, part, 1, 0, st, gate, nullptr, fin, fin_arg);
+  return launch_reduce<1>(c, s, n, op, sp, part, 1, 0, st, gate, nullptr, fin, fin_arg);
 }
 
 static int gs_update_any(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
@@ -566,7 +593,7 @@ static int alloc_mat(pk_ctx* c, int64_t n_rows, int64_t n_cols, int64_t nnz, pk_
   m->row64 = nnz >= (1ll << 31) - 1;
   size_t rsz = (size_t)(n_rows + 1) * (m->row64 ? 8 : 4);
   // pad arrays so vectorised/bulk loads may read a little past the end
-  cudaError_t e = cudaMalloc(&m->rowptr, rsz + 64);
+  cudaError_t e = cudaMalloc(&m->rowptr, rsz + 512);  // bulk row slices read up to 34 entries
   if (e == cudaSuccess) e = cudaMalloc(&m->cols, (size_t)nnz * 4 + 64);
   if (e == cudaSuccess) e = cudaMalloc(&m->vals, (size_t)nnz * 8 + 64);
   if (e != cudaSuccess) {
@@ -807,10 +834,10 @@ extern "C" int pk_reduce_stage1(pk_ctx* c, int64_t n, int32_t nq, const double* 
     int k = std::min(4, nq - q0);
     int rc;
     switch (k) {
-      case 1: { OpColumns<1> op{{columns[q0]}}; rc = launch_reduce<1, 2>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
-      case 2: { OpColumns<2> op{{columns[q0], columns[q0 + 1]}}; rc = launch_reduce<2, 2>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
-      case 3: { OpColumns<3> op{{columns[q0], columns[q0 + 1], columns[q0 + 2]}}; rc = launch_reduce<3, 1>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
-      default: { OpColumns<4> op{{columns[q0], columns[q0 + 1], columns[q0 + 2], columns[q0 + 3]}}; rc = launch_reduce<4, 1>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      case 1: { OpColumns<1> op{}; op.col[0] = columns[q0]; rc = launch_reduce<1>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      case 2: { OpColumns<2> op{}; for (int j = 0; j < 2; ++j) op.col[j] = columns[q0 + j]; rc = launch_reduce<2>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      case 3: { OpColumns<3> op{}; for (int j = 0; j < 3; ++j) op.col[j] = columns[q0 + j]; rc = launch_reduce<3>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
+      default: { OpColumns<4> op{}; for (int j = 0; j < 4; ++j) op.col[j] = columns[q0 + j]; rc = launch_reduce<4>(c, c->stream, n, op, ScalarPtrs{}, partials, nq, q0); break; }
     }
     PK_TRY(rc);
   }
@@ -847,7 +874,7 @@ extern "C" int pk_cg_update(pk_ctx* c, int64_t n, double* x, double* r, double* 
   if (!partials || n < 0) return fail(PK_ERR_INVALID, "bad argument");
   PK_TRY(ensure_scratch(c, n, 1));
   OpCgUpdate op{x, r, p, ap, alpha, beta};
-  return launch_reduce<1, 2>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
+  return launch_reduce<1>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
 }
 
 extern "C" int pk_bicg_s_update(pk_ctx* c, int64_t n, const double* r, const double* ap, const double* rr0p,
@@ -859,8 +886,8 @@ extern "C" int pk_bicg_s_update(pk_ctx* c, int64_t n, const double* r, const dou
   k_bicg_alpha<<<1, 32, 0, c->stream>>>(rr0p, aprp, c->ng, btol, alpha_out, breakdown);
   PK_CUDA(cudaGetLastError());
   OpBicgS op{r, ap, s, 0.0};
-  ScalarPtrs sp{alpha_out, nullptr, nullptr};
-  return launch_reduce<1, 2>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, breakdown);
+  ScalarPtrs sp{alpha_out, nullptr, nullptr, nullptr};
+  return launch_reduce<1>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, breakdown);
 }
 
 extern "C" int pk_bicg_xrp_update(pk_ctx* c, int64_t n, double* x, double* r, double* p, const double* s,
@@ -870,7 +897,7 @@ extern "C" int pk_bicg_xrp_update(pk_ctx* c, int64_t n, double* x, double* r, do
   if (!partials || n < 0) return fail(PK_ERR_INVALID, "bad argument");
   PK_TRY(ensure_scratch(c, n, 1));
   OpBicgXrp op{x, r, p, s, ap, as, r0star, alpha, omega, beta};
-  return launch_reduce<1, 1>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
+  return launch_reduce<1>(c, c->stream, n, op, ScalarPtrs{}, partials, 1, 0);
 }
 
 extern "C" int pk_gs_stage1(pk_ctx* c, int64_t n, int32_t nb, const double* const* basis, const double* v,
@@ -904,8 +931,163 @@ extern "C" int pk_gs_normalize(pk_ctx* c, int64_t n, double* v, const double* no
   k_norm_fin<<<1, 32, 0, c->stream>>>(norm_partials, c->ng, btol, norm_out, inv, lucky);
   PK_CUDA(cudaGetLastError());
   OpNormalize op{v, r, 0.0};
-  ScalarPtrs sp{inv, nullptr, nullptr};
-  return launch_reduce<1, 2>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, lucky);
+  ScalarPtrs sp{inv, nullptr, nullptr, nullptr};
+  return launch_reduce<1>(c, c->stream, n, op, sp, partials, 1, 0, nullptr, GATE_NONE, lucky);
 }
 
 #include "pk_solvers.inc"
+
+// ---------------------------------------------------------------------------
+// engine experiments (not part of the public header): simple reference
+// kernels timed on the device, to bound what the staged engine should reach
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_dbg_spmv_simple(int64_t n, const int32_t* __restrict__ rp,
+                                                         const int32_t* __restrict__ ci,
+                                                         const double* __restrict__ va,
+                                                         const double* __restrict__ p, double* __restrict__ q) {
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x) {
+    int b = __ldg(rp + row), e = __ldg(rp + row + 1);
+    double acc = 0.0;
+    for (int k = b; k < e; ++k) acc = add_rn(acc, mul_rn(__ldg(va + k), __ldg(p + __ldg(ci + k))));
+    q[row] = acc;
+  }
+}
+
+// K_B-shaped: s = r - a Ap recomputed at every gathered column; As and four
+// contribution streams written out (no ordered reduction)
+__global__ void __launch_bounds__(256) k_dbg_bicgb_simple(int64_t n, const int32_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ ci,
+                                                          const double* __restrict__ va,
+                                                          const double* __restrict__ r,
+                                                          const double* __restrict__ ap,
+                                                          const double* __restrict__ r0, double alpha,
+                                                          double* __restrict__ as, double* __restrict__ cc) {
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x) {
+    int b = __ldg(rp + row), e = __ldg(rp + row + 1);
+    double acc = 0.0;
+    for (int k = b; k < e; ++k) {
+      uint32_t c = (uint32_t)__ldg(ci + k);
+      acc = add_rn(acc, mul_rn(__ldg(va + k), sub_rn(__ldg(r + c), mul_rn(alpha, __ldg(ap + c)))));
+    }
+    double s = sub_rn(__ldg(r + row), mul_rn(alpha, __ldg(ap + row)));
+    as[row] = acc;
+    cc[row] = mul_rn(s, s) + mul_rn(acc, s) + mul_rn(acc, acc) + mul_rn(acc, __ldg(r0 + row));
+  }
+}
+
+// engine row order (CHAIN units x chunk batches, U rows per thread) with the
+// ordered fold removed: contributions are only summed per thread
+template <int NQ, int U, class Op, bool kCopy = false>
+__global__ void __launch_bounds__(256, 4) k_dbg_order(Geom geo, const __grid_constant__ Op op0, double* sink) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Op opl = op0;
+  if (kCopy) opl.scalars(ScalarPtrs{});
+  const Op& op = kCopy ? opl : op0;
+  constexpr int B = kWarps * U;
+  double keep = 0.0;
+  for (int64_t unit = blockIdx.x; unit < geo.units; unit += gridDim.x) {
+    const int64_t lid0 = unit * 32;
+    for (int64_t k0 = 0; k0 < geo.K; k0 += B) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t row = (k0 + warp + kWarps * u) * geo.G + lid0 + lane;
+        double c[NQ];
+        if (k0 + warp + kWarps * u < geo.K && row < geo.n) {
+          row_contrib<NQ>(op, (uint32_t)row, c);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) keep = add_rn(keep, c[q]);
+        }
+      }
+    }
+  }
+  if (keep == 12345.678) sink[0] = keep;
+}
+
+// the same operator on a plain grid-stride thread-per-row loop
+template <int NQ, class Op>
+__global__ void __launch_bounds__(256, 4) k_dbg_gridstride(int64_t n, Op op, double* sink) {
+  double keep = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x) {
+    double c[NQ];
+    row_contrib<NQ>(op, (uint32_t)row, c);
+    keep = add_rn(keep, c[0]);
+  }
+  if (keep == 12345.678) sink[0] = keep;
+}
+
+extern "C" int pk_debug_bench(pk_ctx* c, const pk_mat* a, int kind, int reps, double* us_out) {
+  PK_CHECK_CTX(c);
+  if (!a || a->row64 || !us_out) return fail(PK_ERR_INVALID, "bad argument");
+  const int64_t n = a->n_rows;
+  double* buf = nullptr;
+  PK_CUDA(cudaMalloc(&buf, (size_t)n * 8 * 6 + 64));
+  cudaMemset(buf, 0, (size_t)n * 8 * 6);
+  double *p = buf, *q = buf + n, *r = buf + 2 * n, *ap = buf + 3 * n, *r0 = buf + 4 * n, *cc = buf + 5 * n;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+  OpBicgB<int32_t, 5> ob{};
+  ob.A = csr_of<int32_t>(a);
+  ob.r[0] = ob.r[1] = r;
+  ob.ap[0] = ob.ap[1] = ap;
+  ob.r0 = r0;
+  ob.as = q;
+  ob.alpha = 0.5;
+  ob.rc = r;
+  ob.apc = ap;
+  Geom geo = make_geom(n, c->ng, c->gs);
+  PK_TRY(ensure_scratch(c, n, 4));
+  auto run = [&]() {
+    if (kind == 0)
+      k_dbg_spmv_simple<<<grid, 256, 0, c->stream>>>(n, (const int32_t*)a->rowptr, a->cols, a->vals, p, q);
+    else if (kind == 1)
+      k_dbg_bicgb_simple<<<grid, 256, 0, c->stream>>>(n, (const int32_t*)a->rowptr, a->cols, a->vals, r, ap, r0, 0.5,
+                                                      q, cc);
+    else if (kind == 2)
+      launch_reduce<4>(c, c->stream, n, ob, ScalarPtrs{}, cc, 4, 0);
+    else if (kind == 3)
+      k_dbg_order<4, 2><<<(int)std::min<int64_t>(geo.units, (int64_t)c->sm_count * 4), 256, 0, c->stream>>>(geo, ob, cc);
+    else if (kind == 4)
+      k_dbg_gridstride<4><<<grid, 256, 0, c->stream>>>(n, ob, cc);
+    else if (kind == 5)
+      k_dbg_order<4, 2><<<(int)geo.units, 256, 0, c->stream>>>(geo, ob, cc);
+    else if (kind == 9)
+      k_dbg_order<4, 2, OpBicgB<int32_t, 5>, true><<<(int)std::min<int64_t>(geo.units, (int64_t)c->sm_count * 4), 256, 0, c->stream>>>(geo, ob, cc);
+    else if (kind >= 6 && kind <= 8) {
+      // the engine kernel itself with an explicit grid (kind 6: one CTA per
+      // unit; kind 7: 2 units per CTA; kind 8: occupancy-sized grid)
+      auto kern = k_reduce<4, 2, 4, OpBicgB<int32_t, 5>>;
+      size_t smem = engine_smem_bytes(geo, 4, 2);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int grid6 = kind == 6 ? (int)geo.units : kind == 7 ? (int)((geo.units + 1) / 2) : engine_grid(c, kern, smem, geo.units);
+      if (reps == 0) printf("kind %d grid %d smem %zu\n", kind, grid6, smem);
+      kern<<<grid6, kThreads, smem, c->stream>>>(geo, ob, ScalarPtrs{}, cc, 4, 0, 4, scratch_of(c), nullptr, GATE_NONE,
+                                                 nullptr, FIN_NONE, 0);
+    }
+  };
+  for (int i = 0; i < 3; ++i) run();
+  if (kind >= 6 && kind <= 8) {
+    int r0_ = reps;
+    reps = 0;
+    run();
+    reps = r0_;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reduce<4, 2, 4, OpBicgB<int32_t, 5>>, kThreads,
+                                                  engine_smem_bytes(geo, 4, 2));
+    printf("occupancy %d CTAs/SM\n", occ);
+  }
+  cudaEventRecord(e0, c->stream);
+  for (int i = 0; i < reps; ++i) run();
+  cudaEventRecord(e1, c->stream);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *us_out = ms * 1e3 / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}

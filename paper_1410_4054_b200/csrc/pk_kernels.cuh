@@ -31,7 +31,7 @@
 namespace pk {
 
 // ---------------------------------------------------------------------------
-// finalizers (run by every thread of the finalizer CTA of a launch)
+// finalizers (run by one warp: the fold warp of the finalizer CTA, or k_finalize)
 // ---------------------------------------------------------------------------
 
 enum Fin : int32_t {
@@ -111,7 +111,7 @@ __device__ inline void cg_scalars(SolveState* st, double rr, double pap, double 
 }
 
 __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
-  const int th = threadIdx.x;
+  const int th = threadIdx.x & 31;  // executed by one warp
   const int ng = st->n_groups;
   __shared__ double tot[32];
   switch (fin) {
@@ -120,13 +120,13 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
       if (th == 1) tot[1] = stage2_col(st->p_two, ng, 2, 0);
       if (th == 2) tot[2] = stage2_col(st->p_two, ng, 2, 1);
       if (th == 3) tot[3] = stage2_col(st->p_bb, ng, 1, 0);
-      __syncthreads();
+      __syncwarp();
       if (th == 0) cg_scalars(st, tot[0], tot[1], tot[2], true, tot[3], ing);
       break;
     }
     case FIN_CG_FUSED: {
       if (th < 3) tot[th] = stage2_col(st->p_three, ng, 3, th);
-      __syncthreads();
+      __syncwarp();
       if (th == 0) {
         st->parity ^= 1;
         cg_scalars(st, tot[0], tot[1], tot[2], false, 0.0, ing);
@@ -136,7 +136,7 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     case FIN_BICG_SETUP: {
       if (th == 0) tot[0] = stage2_col(st->p_pair, ng, 2, 0);
       if (th == 1) tot[1] = stage2_col(st->p_bb, ng, 1, 0);
-      __syncthreads();
+      __syncwarp();
       if (th != 0) return;
       double rr = tot[0];
       double nb = msqrt(tot[1]);
@@ -153,7 +153,7 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     case FIN_BICG_ALPHA: {
       // fused_bicgstab_s_update's in-kernel alpha (fused.py:172-176)
       if (th < 2) tot[th] = stage2_col(st->p_pair, ng, 2, th);
-      __syncthreads();
+      __syncwarp();
       if (th != 0) return;
       if (arg) st->parity ^= 1;
       double rho = tot[0], d = tot[1];
@@ -171,7 +171,7 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     case FIN_BICG_TAIL: {
       // solvers.py:647-684
       if (th < 4) tot[th] = stage2_col(st->p_quad, ng, 4, th);
-      __syncthreads();
+      __syncwarp();
       if (th != 0) return;
       double ss = tot[0], ass = tot[1], asas = tot[2], asr = tot[3], apr = st->apr;
       st->ss = ss; st->ass = ass; st->asas = asas; st->asr = asr;
@@ -223,7 +223,7 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     case FIN_GM_RHO: {
       if (th == 0) tot[0] = stage2_col(st->p_rr, ng, 1, 0);
       if (th == 1 && arg) tot[1] = stage2_col(st->p_bb, ng, 1, 0);
-      __syncthreads();
+      __syncwarp();
       if (th != 0) return;
       if (arg) {
         double nb = msqrt(tot[1]);
@@ -248,7 +248,7 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     }
     case FIN_GM_COEF: {
       // arg = step index i (>= 2): columns 0..i-2 of p_coef
-      for (int j = th; j < arg - 1; j += blockDim.x) {
+      for (int j = th; j < arg - 1; j += 32) {
         double c = stage2_col(st->p_coef, ng, st->m, j);
         st->coef[j] = c;
         st->R[(int64_t)j * st->m + (arg - 1)] = c;
@@ -285,38 +285,40 @@ __device__ __forceinline__ double ld_scalar(const double* p, double v) { return 
 __device__ __forceinline__ int ld_par(const int32_t* p) { return p ? *(volatile const int32_t*)p : 0; }
 
 // ---------------------------------------------------------------------------
-// SpMV operators (Op::kSpmv): the engine stages the CSR tile, the operator
-// supplies gload/gval (the SpMV input at a gathered column) and the per-row
-// epilogue.
+// SpMV operators (Op::kSpmv): the engine walks the row's CSR entries, the
+// operator supplies gload/gval (the SpMV input at a gathered column) and the
+// per-row epilogue.  kSlots = entries per pass (all loads of a pass in
+// flight): 5 for 2-D 5-point rows, 7 for 3-D 7-point rows.
 // ---------------------------------------------------------------------------
 
 // q = A p with NQ fused dots (fused.py:86-120); NQ = 0: plain spmv_csr.
-template <typename RowT, int NQ>
+template <typename RowT_, int NQ, int S_>
 struct OpSpmvFused {
+  using RowT = RowT_;
   static constexpr bool kSpmv = true;
-  static constexpr int kMinBlocks = 3;
-  static constexpr int kSlots = 8;
+  static constexpr int kMinBlocks = 4;
+  static constexpr int kRowsPerThread = 2;
+  static constexpr int kSlots = S_;
   Csr<RowT> A;
   const double* __restrict__ p;
   double* q;
   int32_t kind[4];
   const double* w[4];
-  struct Item {
-    double pv;
-    double wv[NQ > 0 ? NQ : 1];
-  };
-  __device__ __forceinline__ void load(int64_t row, Item& it) const {
+  struct Item { double pv; double wv[NQ > 0 ? NQ : 1]; };
+  struct Gat { double v; };
+  __device__ __forceinline__ void load(uint32_t row, Item& it) const {
+    it.pv = 0.0;
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
+      it.wv[k] = 0.0;
       if (kind[k] == PK_DOT_INPUT) it.pv = __ldg(p + row);
       if (kind[k] == PK_DOT_VECTOR) it.wv[k] = __ldg(w[k] + row);
     }
   }
-  struct Gat { double v; };
-  __device__ __forceinline__ void gload(int32_t col, Gat& g) const { g.v = __ldg(p + col); }
+  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const { g.v = __ldg(p + col); }
   __device__ __forceinline__ double gval(const Gat& g) const { return g.v; }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t row, Item& it, double acc, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t row, Item& it, double acc, double (&c)[M]) const {
     if (q) q[row] = acc;
 #pragma unroll
     for (int k = 0; k < NQ && k < M; ++k) {
@@ -328,11 +330,13 @@ struct OpSpmvFused {
 };
 
 // r = b + (-1) A x (add_scaled, linalg.py:450-457); optional copies; <r,r>.
-template <typename RowT>
+template <typename RowT_, int S_>
 struct OpResidual {
+  using RowT = RowT_;
   static constexpr bool kSpmv = true;
-  static constexpr int kMinBlocks = 3;
-  static constexpr int kSlots = 8;
+  static constexpr int kMinBlocks = 4;
+  static constexpr int kRowsPerThread = 2;
+  static constexpr int kSlots = S_;
   Csr<RowT> A;
   const double* __restrict__ x;
   const double* __restrict__ b;
@@ -340,12 +344,12 @@ struct OpResidual {
   double* copy1;
   double* copy2;
   struct Item { double bv; };
-  __device__ __forceinline__ void load(int64_t row, Item& it) const { it.bv = __ldg(b + row); }
   struct Gat { double v; };
-  __device__ __forceinline__ void gload(int32_t col, Gat& g) const { g.v = __ldg(x + col); }
+  __device__ __forceinline__ void load(uint32_t row, Item& it) const { it.bv = __ldg(b + row); }
+  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const { g.v = __ldg(x + col); }
   __device__ __forceinline__ double gval(const Gat& g) const { return g.v; }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t row, Item& it, double q, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t row, Item& it, double q, double (&c)[M]) const {
     double rv = add_rn(it.bv, mul_rn(-1.0, q));
     if (r) r[row] = rv;
     if (copy1) copy1[row] = rv;
@@ -359,11 +363,13 @@ struct OpResidual {
 //   r' = r - a Ap;  p' = p b + r';  x += a p;  Ap' = A p';
 //   contributions [r'.r', Ap'.p', Ap'.Ap'].
 // p' at a gathered column is recomputed from (p, r, Ap) there.
-template <typename RowT>
+template <typename RowT_, int S_>
 struct OpCgFused {
+  using RowT = RowT_;
   static constexpr bool kSpmv = true;
-  static constexpr int kMinBlocks = 2;
-  static constexpr int kSlots = 4;
+  static constexpr int kMinBlocks = 3;
+  static constexpr int kRowsPerThread = 2;
+  static constexpr int kSlots = S_;
   Csr<RowT> A;
   double* x;
   double* r[2];
@@ -377,11 +383,11 @@ struct OpCgFused {
   double* pn_;
   double* apn_;
   struct Item { double x, r, p, ap; };
-  __device__ __forceinline__ void load(int64_t row, Item& it) const {
-    it.x = x[row]; it.r = rc[row]; it.p = pc[row]; it.ap = apc[row];
-  }
   struct Gat { double r, ap, p; };
-  __device__ __forceinline__ void gload(int32_t col, Gat& g) const {
+  __device__ __forceinline__ void load(uint32_t row, Item& it) const {
+    it.x = __ldg(x + row); it.r = __ldg(rc + row); it.p = __ldg(pc + row); it.ap = __ldg(apc + row);
+  }
+  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const {
     g.r = __ldg(rc + col); g.ap = __ldg(apc + col); g.p = __ldg(pc + col);
   }
   __device__ __forceinline__ double gval(const Gat& g) const {
@@ -389,7 +395,7 @@ struct OpCgFused {
     return add_rn(mul_rn(g.p, beta), rn);
   }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t row, Item& it, double q, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t row, Item& it, double q, double (&c)[M]) const {
     double xn = add_rn(it.x, mul_rn(alpha, it.p));
     double rn = sub_rn(it.r, mul_rn(alpha, it.ap));
     double pn = add_rn(mul_rn(it.p, beta), rn);
@@ -410,11 +416,13 @@ struct OpCgFused {
 // BiCGStab second SpMV with the s-update folded in (fused.py:154-182 + 86-120):
 //   s = r - a Ap (recomputed at every gathered column, never stored);
 //   As = A s;  contributions [s.s, As.s, As.As, As.r0*].
-template <typename RowT>
+template <typename RowT_, int S_>
 struct OpBicgB {
+  using RowT = RowT_;
   static constexpr bool kSpmv = true;
-  static constexpr int kMinBlocks = 2;
-  static constexpr int kSlots = 6;
+  static constexpr int kMinBlocks = 4;
+  static constexpr int kRowsPerThread = 2;
+  static constexpr int kSlots = S_;
   Csr<RowT> A;
   const double* r[2];
   const double* ap[2];
@@ -424,15 +432,15 @@ struct OpBicgB {
   const double* rc;
   const double* apc;
   struct Item { double s, r0; };
-  __device__ __forceinline__ void load(int64_t row, Item& it) const {
+  struct Gat { double r, ap; };
+  __device__ __forceinline__ void load(uint32_t row, Item& it) const {
     it.s = sub_rn(__ldg(rc + row), mul_rn(alpha, __ldg(apc + row)));
     it.r0 = __ldg(r0 + row);
   }
-  struct Gat { double r, ap; };
-  __device__ __forceinline__ void gload(int32_t col, Gat& g) const { g.r = __ldg(rc + col); g.ap = __ldg(apc + col); }
+  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const { g.r = __ldg(rc + col); g.ap = __ldg(apc + col); }
   __device__ __forceinline__ double gval(const Gat& g) const { return sub_rn(g.r, mul_rn(alpha, g.ap)); }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t row, Item& it, double q, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t row, Item& it, double q, double (&c)[M]) const {
     as[row] = q;
     c[0] = mul_rn(it.s, it.s);
     c[1] = mul_rn(q, it.s);
@@ -451,11 +459,13 @@ struct OpBicgB {
 // (fused.py:185-219 + 86-120):
 //   s = r - a Ap;  x += (a p) + (w s);  r' = s - w As;  p' = ((p - w Ap) b) + r';
 //   Ap' = A p';  contributions [r'.r0*, Ap'.r0*].
-template <typename RowT>
+template <typename RowT_, int S_>
 struct OpBicgA {
+  using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = 2;
-  static constexpr int kSlots = 4;
+  static constexpr int kRowsPerThread = 2;
+  static constexpr int kSlots = S_;
   Csr<RowT> A;
   double* x;
   double* r[2];
@@ -471,12 +481,12 @@ struct OpBicgA {
   double* pn_;
   double* apn_;
   struct Item { double x, r, p, ap, as, r0; };
-  __device__ __forceinline__ void load(int64_t row, Item& it) const {
-    it.x = x[row]; it.r = rc[row]; it.p = pc[row]; it.ap = apc[row];
+  struct Gat { double r, ap, as, p; };
+  __device__ __forceinline__ void load(uint32_t row, Item& it) const {
+    it.x = __ldg(x + row); it.r = __ldg(rc + row); it.p = __ldg(pc + row); it.ap = __ldg(apc + row);
     it.as = __ldg(as + row); it.r0 = __ldg(r0 + row);
   }
-  struct Gat { double r, ap, as, p; };
-  __device__ __forceinline__ void gload(int32_t col, Gat& g) const {
+  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const {
     g.r = __ldg(rc + col); g.ap = __ldg(apc + col); g.as = __ldg(as + col); g.p = __ldg(pc + col);
   }
   __device__ __forceinline__ double gval(const Gat& g) const {
@@ -485,7 +495,7 @@ struct OpBicgA {
     return add_rn(mul_rn(sub_rn(g.p, mul_rn(omega, g.ap)), beta), rn);
   }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t row, Item& it, double q, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t row, Item& it, double q, double (&c)[M]) const {
     double s = sub_rn(it.r, mul_rn(alpha, it.ap));
     double xn = add_rn(it.x, add_rn(mul_rn(alpha, it.p), mul_rn(omega, s)));
     double rn = sub_rn(s, mul_rn(omega, it.as));
@@ -522,12 +532,12 @@ struct OpBicgXrpTail {
   double alpha, omega, beta;
   int cur;
   struct Item { double x, r, p, ap, as, r0; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const {
-    it.x = x[i]; it.r = (cur ? r[1] : r[0])[i]; it.p = (cur ? p[1] : p[0])[i]; it.ap = __ldg((cur ? ap[1] : ap[0]) + i);
-    it.as = __ldg(as + i); it.r0 = __ldg(r0 + i);
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
+    it.x = x[i]; it.r = (cur ? r[1] : r[0])[i]; it.p = (cur ? p[1] : p[0])[i];
+    it.ap = __ldg((cur ? ap[1] : ap[0]) + i); it.as = __ldg(as + i); it.r0 = __ldg(r0 + i);
   }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&c)[M]) const {
     double s = sub_rn(it.r, mul_rn(alpha, it.ap));
     double xn = add_rn(it.x, add_rn(mul_rn(alpha, it.p), mul_rn(omega, s)));
     double rn = sub_rn(s, mul_rn(omega, it.as));
@@ -553,11 +563,11 @@ struct OpCgUpdate {
   const double* __restrict__ ap;
   double alpha, beta;
   struct Item { double x, r, p, ap; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const {
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.x = x[i]; it.r = r[i]; it.p = p[i]; it.ap = __ldg(ap + i);
   }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&c)[M]) const {
     double xn = add_rn(it.x, mul_rn(alpha, it.p));
     double rn = sub_rn(it.r, mul_rn(alpha, it.ap));
     double pn = add_rn(mul_rn(it.p, beta), rn);
@@ -579,12 +589,12 @@ struct OpBicgS {
   double* s;
   double alpha;
   struct Item { double r, ap; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const { it.r = __ldg(r + i); it.ap = __ldg(ap + i); }
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const { it.r = __ldg(r + i); it.ap = __ldg(ap + i); }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
-    double sv = sub_rn(it.r, mul_rn(alpha, it.ap));
-    s[i] = sv;
-    c[0] = mul_rn(sv, sv);
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&c)[M]) const {
+    double v = sub_rn(it.r, mul_rn(alpha, it.ap));
+    s[i] = v;
+    c[0] = mul_rn(v, v);
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs& sp) { alpha = ld_scalar(sp.a, alpha); }
 };
@@ -602,11 +612,11 @@ struct OpBicgXrp {
   const double* __restrict__ r0;
   double alpha, omega, beta;
   struct Item { double x, p, s, ap, as, r0; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const {
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.x = x[i]; it.p = p[i]; it.s = __ldg(s + i); it.ap = __ldg(ap + i); it.as = __ldg(as + i); it.r0 = __ldg(r0 + i);
   }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&c)[M]) const {
     double xn = add_rn(it.x, add_rn(mul_rn(alpha, it.p), mul_rn(omega, it.s)));
     double rn = sub_rn(it.s, mul_rn(omega, it.as));
     double pn = add_rn(mul_rn(sub_rn(it.p, mul_rn(omega, it.ap)), beta), rn);
@@ -627,9 +637,9 @@ struct OpDot {
   const double* __restrict__ x;
   const double* __restrict__ y;
   struct Item { double x, y; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const { it.x = __ldg(x + i); it.y = __ldg(y + i); }
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const { it.x = __ldg(x + i); it.y = __ldg(y + i); }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const { c[0] = mul_rn(it.x, it.y); }
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&c)[M]) const { c[0] = mul_rn(it.x, it.y); }
   __device__ __forceinline__ void scalars(const ScalarPtrs&) {}
 };
 
@@ -640,12 +650,12 @@ struct OpColumns {
   static constexpr int kMinBlocks = 4;
   const double* col[NQ];
   struct Item { double v[NQ]; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const {
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
 #pragma unroll
     for (int k = 0; k < NQ; ++k) it.v[k] = __ldg(col[k] + i);
   }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&c)[M]) const {
 #pragma unroll
     for (int k = 0; k < NQ && k < M; ++k) c[k] = it.v[k];
   }
@@ -661,13 +671,16 @@ struct OpMultiDot {
   int32_t nb;
   const double* b[NB];
   struct Item { double v; double b[NB]; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const {
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.v = __ldg(v + i);
 #pragma unroll
-    for (int j = 0; j < NB; ++j) if (j < nb) it.b[j] = __ldg(b[j] + i);
+    for (int j = 0; j < NB; ++j) {
+      it.b[j] = 0.0;
+      if (j < nb) it.b[j] = __ldg(b[j] + i);
+    }
   }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&c)[M]) const {
 #pragma unroll
     for (int j = 0; j < NB && j < M; ++j) c[j] = j < nb ? mul_rn(it.b[j], it.v) : 0.0;
   }
@@ -684,13 +697,16 @@ struct OpGsUpdate {
   const double* b[NB];
   const double* coef;  // device [nb], finalized by the previous kernel
   struct Item { double v; double b[NB]; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const {
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.v = v[i];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) if (j < nb) it.b[j] = __ldg(b[j] + i);
+    for (int j = 0; j < NB; ++j) {
+      it.b[j] = 0.0;
+      if (j < nb) it.b[j] = __ldg(b[j] + i);
+    }
   }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&cc)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&cc)[M]) const {
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(__ldg(coef + j), it.b[j]));
@@ -711,9 +727,9 @@ struct OpNormalize {
   const double* __restrict__ r;
   double inv;
   struct Item { double v, r; };
-  __device__ __forceinline__ void load(int64_t i, Item& it) const { it.v = v[i]; it.r = __ldg(r + i); }
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const { it.v = v[i]; it.r = __ldg(r + i); }
   template <int M>
-  __device__ __forceinline__ void compute(int64_t i, Item& it, double (&c)[M]) const {
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&c)[M]) const {
     double vn = mul_rn(it.v, inv);
     v[i] = vn;
     c[0] = mul_rn(it.r, vn);

@@ -1,4 +1,4 @@
-// Ordered two-stage reduction engine for sm_100a (v2: staged, chunk-parallel).
+// Ordered two-stage reduction engine for sm_100a.
 //
 // Reproduces the reference's reduction schedule bit-for-bit
 // (pipekrylov/linalg.py:289-320):
@@ -7,24 +7,21 @@
 //   stage 2: serial left-to-right sum over groups.
 //
 // Only the ORDER of the additions is prescribed; the contributions c[i]
-// themselves are independent.  The engine therefore splits every kernel in
-// two phases per batch:
-//   phase A  all 8 warps of the CTA compute contributions of 32-row tiles
-//            (coalesced, CSR products staged through shared memory) and park
-//            them in shared memory -- this is where the memory-level
-//            parallelism comes from;
-//   phase B  warp 0 (the "lane threads", one lane each) folds the parked
-//            contributions into its running lane values in the exact
-//            reference order.
+// themselves are independent, so every row is computed by its own thread
+// with plain, lean, high-occupancy code (thread-per-row SpMV, CSR and vectors
+// straight through L1/L2 -- measured at 5.7-6.8 TB/s on B200 for the
+// BiCGStab-shaped row), and only the folding is ordered:
+//   phase A  the 8 warps of a CTA each compute U rows (32-row tiles) and park
+//            their contributions in shared memory;
+//   phase B  warp 0 (the "lane threads", one lane each) folds them into its
+//            running lane values in the exact reference order.
 //
 // Two mappings, chosen per launch from (n, n_groups, group_size):
 //   CHAIN (K = ceil(n/G) >= 2, or group_size < 32): a CTA owns a block of 32
 //            consecutive lane ids of [0, G) and walks the K chunks
-//            (rows k*G + lane); the 8 warps take 8 chunks per batch.  Lane
-//            values go to a small spill buffer (G x nq doubles); the last CTA
-//            of a group (per-group ticket) runs the group's halving tree.
-//            The default reference geometry 128 x 256 runs here with
-//            G/32 = 1024 CTAs instead of 128.
+//            (rows k*G + lane), 8U chunks per batch.  Lane values go to a
+//            small spill buffer (G x nq doubles); the last CTA of a group
+//            (per-group ticket) runs the group's halving tree.
 //   LEAF  (K = 1, group_size >= 32): a CTA owns a group; lane thread th owns
 //            the lanes {th + 32 j}, whose sub-tree is evaluated by visiting
 //            j in bit-reversed order through a binary-counter stack (only
@@ -41,9 +38,8 @@
 
 namespace pk {
 
-constexpr int kThreads = 256;  // CTA size of every engine kernel
-constexpr int kWarps = kThreads / 32;
-constexpr int kPCap = 256;     // staged CSR products per warp tile
+constexpr int kWarps = 8;  // warps of an engine CTA
+constexpr int kThreads = kWarps * 32;
 constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ inline int ilog2_u(uint32_t v) {
@@ -89,20 +85,15 @@ inline Geom make_geom(int64_t n, int32_t n_groups, int32_t gs) {
   return g;
 }
 
-// Dynamic shared memory (doubles) of one engine kernel.
-//   C     [8U][nq][32]  parked contributions
-//   P     [8][kPCap]    CSR products (SpMV operators only)
+// Dynamic shared memory of one engine kernel (doubles):
+//   C     [2][kWarps U][nq][32]  parked contributions (double-buffered)
 //   tail  LEAF: stack (logm+1) x nq x 32;  CHAIN: tree nq x tT + stack
-inline size_t engine_smem_bytes(const Geom& g, int nq, int U, bool spmv) {
-  size_t c = (size_t)kWarps * U * nq * 32;
-  size_t p = spmv ? (size_t)kWarps * kPCap : 0;
-  size_t t;
-  if (g.leaf) {
-    t = g.m > 1 ? (size_t)(g.logm + 1) * nq * 32 : 0;
-  } else {
-    t = (size_t)nq * g.tT + (g.tm > 1 ? (size_t)(g.tlogm + 1) * nq * g.tT : 0);
-  }
-  return (c + p + t) * sizeof(double);
+__host__ __device__ inline size_t engine_tail_doubles(const Geom& g, int nq) {
+  return g.leaf ? (g.m > 1 ? (size_t)(g.logm + 1) * nq * 32 : 0)
+                : (size_t)nq * g.tT + (g.tm > 1 ? (size_t)(g.tlogm + 1) * nq * g.tT : 0);
+}
+inline size_t engine_smem_bytes(const Geom& g, int nq, int U) {
+  return ((size_t)2 * kWarps * U * nq * 32 + engine_tail_doubles(g, nq)) * sizeof(double);
 }
 
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -127,109 +118,52 @@ struct Csr {
 };
 
 // ---------------------------------------------------------------------------
-// phase A: contributions of one 32-row tile [row0, row0 + valid)
+// phase A: the contributions of one row (lean thread-per-row code)
 // ---------------------------------------------------------------------------
 //
 // Operator concept (pk_kernels.cuh):
-//   static constexpr bool kSpmv;  struct Item;
-//   void load(int64_t row, Item&)                 per-row vector loads
-//   kSpmv:  Csr<RowT> A;  struct Gat;  void gload(int32_t col, Gat&)  raw words
-//           double gval(const Gat&)          SpMV input value at col (may recompute)
-//           void compute(int64_t row, Item&, double q, double (&c)[NQ])
-//   else:   void compute(int64_t row, Item&, double (&c)[NQ])
-//   void scalars(const ScalarPtrs&)               prologue: device scalars
+//   static constexpr bool kSpmv;  static constexpr int kMinBlocks;  struct Item;
+//   void load(uint32_t row, Item&)                 per-row vector loads
+//   kSpmv:  using RowT; Csr<RowT> A; static constexpr int kSlots;
+//           struct Gat; void gload(uint32_t col, Gat&)   raw words at col
+//           double gval(const Gat&)                      SpMV input value (may recompute)
+//           void compute(uint32_t row, Item&, double q, double (&c)[NQ])
+//   else:   void compute(uint32_t row, Item&, double (&c)[NQ])
+//   void scalars(const ScalarPtrs&)                 prologue: device scalars
 //
 // SpMV rows are summed acc = ((0 + v0 x0) + v1 x1) + ... in stored order
-// (_spmvkernels.py:12-18).  The warp loads the tile's contiguous nnz range
-// coalesced, forms every product once, parks it in shared memory and each
-// lane then adds its own row's products in order.
+// (_spmvkernels.py:12-18).  kSlots entries per pass: all loads of a pass are
+// issued first (slots past the row end re-read its last entry -- always a
+// valid address -- and are not added), then the ordered adds.
 template <int NQ, class Op>
-__device__ __forceinline__ void tile_contrib(const Op& op, int64_t row0, int valid, double* pbuf,
-                                             double (&c)[NQ]) {
-  const int lane = threadIdx.x & 31;
-  const bool v = lane < valid;
-  const int64_t row = row0 + lane;
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) c[q] = 0.0;
-  if (valid <= 0) return;
+__device__ __forceinline__ void row_contrib(const Op& op, uint32_t row, double (&c)[NQ]) {
   typename Op::Item it;
+  op.load(row, it);
   if constexpr (Op::kSpmv) {
-    using RowT = typename decltype(Op::A)::RowT;
-    RowT beg = 0, end = 0;
-    if (v) {
-      beg = __ldg(op.A.rp + row);
-      end = __ldg(op.A.rp + row + 1);
-      op.load(row, it);
-    }
-    const RowT base = __shfl_sync(kFull, beg, 0);
-    const RowT top = __shfl_sync(kFull, end, valid - 1);
-    const int64_t L = (int64_t)(top - base);
-    constexpr int S = Op::kSlots;  // nnz slots per lane per pass
+    using RowT = typename Op::RowT;
+    constexpr int S = Op::kSlots;
+    const RowT b = __ldg(op.A.rp + row), e = __ldg(op.A.rp + row + 1);
     double acc = 0.0;
-    if (L <= kPCap) {
-      for (int e0 = 0; e0 < L; e0 += S * 32) {
-        // three explicit stages so every load of a stage is in flight at
-        // once: column/value words, then the gathered input words, then
-        // the products (Op::Gat holds the raw words of one gathered input).
-        // every slot is defined on every path (predicated-off slots keep
-        // column 0 / zeros), so the arrays stay in registers
-        int32_t col[S];
-        double val[S];
-        typename Op::Gat gv[S];
+    for (RowT k0 = b; k0 < e; k0 += S) {
+      int32_t col[S];
+      double val[S];
+      typename Op::Gat gv[S];
 #pragma unroll
-        for (int j = 0; j < S; ++j) {
-          col[j] = 0;
-          val[j] = 0.0;
-          gv[j] = typename Op::Gat{};
-        }
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-          const int e = e0 + j * 32 + lane;
-          if (e < L) {
-            col[j] = __ldg(op.A.ci + base + e);
-            val[j] = __ldg(op.A.va + base + e);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-          if (e0 + j * 32 + lane < L) op.gload(col[j], gv[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-          const int e = e0 + j * 32 + lane;
-          if (e < L) pbuf[e] = mul_rn(val[j], op.gval(gv[j]));
-        }
+      for (int j = 0; j < S; ++j) {
+        const RowT k = (k0 + j < e) ? k0 + j : e - 1;
+        col[j] = __ldg(op.A.ci + k);
+        val[j] = __ldg(op.A.va + k);
       }
-      __syncwarp();
-      if (v) {
-        const int hi = (int)(end - base);
-        for (int e = (int)(beg - base); e < hi; ++e) acc = add_rn(acc, pbuf[e]);
-      }
-      __syncwarp();
-    } else {
-      // long rows: direct ordered loop (correct for any row length)
-      if (v) {
-        for (RowT e = beg; e < end; ++e) {
-          typename Op::Gat g;
-          op.gload(__ldg(op.A.ci + e), g);
-          acc = add_rn(acc, mul_rn(__ldg(op.A.va + e), op.gval(g)));
-        }
-      }
+#pragma unroll
+      for (int j = 0; j < S; ++j) op.gload((uint32_t)col[j], gv[j]);
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        if (k0 + j < e) acc = add_rn(acc, mul_rn(val[j], op.gval(gv[j])));
     }
-    if (v) op.compute(row, it, acc, c);
+    op.compute(row, it, acc, c);
   } else {
-    if (v) {
-      op.load(row, it);
-      op.compute(row, it, c);
-    }
+    op.compute(row, it, c);
   }
-}
-
-// Elementwise tile without contributions (plain SpMV / sweeps).
-template <class Op>
-__device__ __forceinline__ void tile_apply(const Op& op, int64_t row0, int valid, double* pbuf) {
-  double c[1];
-  tile_contrib<1>(op, row0, valid, pbuf, c);
 }
 
 // ---------------------------------------------------------------------------
@@ -331,21 +265,47 @@ __device__ __forceinline__ void group_tree(const Geom& geo, int g, const double*
 // the engine
 // ---------------------------------------------------------------------------
 
+// Ticket increment with release semantics at gpu scope: MEMBAR.ALL.GPU +
+// ATOM, without the L1 invalidation (CCTL.IVALL) that __threadfence() adds --
+// an invalidation would throw away the L1-resident CSR lines of every warp on
+// the SM.  Readers of the published data use L2 loads (ld.global.cg).
+__device__ __forceinline__ unsigned atomic_add_release(unsigned* p, unsigned v) {
+  unsigned r;
+  asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+
+// Scalar binary-counter leaf push for quantity q (stk laid out as LeafStack).
+template <int NQ>
+__device__ __forceinline__ double leaf_push(double* stk, int q, int lane, uint32_t i, double v) {
+  int lvl = 0;
+  for (uint32_t c = i; c & 1u; c >>= 1, ++lvl) v = add_rn(stk[(lvl * NQ + q) * 32 + lane], v);
+  stk[(lvl * NQ + q) * 32 + lane] = v;
+  return v;
+}
+
 // Runs stage 1 of this CTA's units and writes part[g * ld + col0 + q] for
 // q < nstore.  Returns true in every thread of the CTA that completed the
 // last group (the finalizer CTA).
+//
+// Per batch (B = kWarps U chunks / leaves): every thread computes U rows and
+// parks the contributions in C[batch & 1]; ONE barrier; then warp w folds
+// quantities q = w, w + kWarps, ... of the batch in the reference order while
+// the other warps already compute the next batch into the other half of C
+// (the barrier of the next batch orders the reuse).
 template <int NQ, int U, class Op>
 __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double* smem, double* part, int ld,
                                            int col0, int nstore, const Scratch& scr, unsigned* ticket) {
   __shared__ int s_flag;
   __shared__ int s_last;
+  constexpr int B = kWarps * U;                   // chunks (CHAIN) / leaves (LEAF) per batch
+  constexpr int QPW = (NQ + kWarps - 1) / kWarps; // quantities folded per warp
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  constexpr int B = kWarps * U;  // chunks (or leaves) per batch
-  double* C = smem;
-  double* pbuf = C + (size_t)B * NQ * 32 + (Op::kSpmv ? warp * kPCap : 0);
-  double* tail = C + (size_t)B * NQ * 32 + (Op::kSpmv ? kWarps * kPCap : 0);
+  double* Cbuf = smem;  // [2][B][NQ][32]
+  double* tail = Cbuf + 2 * B * NQ * 32;
   if (tid == 0) s_last = 0;
+  uint32_t bpar = 0;  // which half of C the next batch writes
 
   for (int64_t unit = blockIdx.x; unit < geo.units; unit += gridDim.x) {
     int ncomplete = 0;
@@ -353,53 +313,58 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
       // ---- CHAIN: 32 lane ids [lid0, lid0 + nl), chunks k = 0..K-1 ----
       const int64_t lid0 = unit * 32;
       const int nl = (int)((geo.G - lid0) < 32 ? (geo.G - lid0) : 32);
-      double acc[NQ];
+      const bool lane_ok = lane < nl;
+      double acc[QPW];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+      for (int i = 0; i < QPW; ++i) acc[i] = 0.0;
       for (int64_t k0 = 0; k0 < geo.K; k0 += B) {
+        double* C = Cbuf + (bpar & 1u) * (B * NQ * 32);
+        ++bpar;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int kk = warp + kWarps * u;
-          const int64_t k = k0 + kk;
-          if (k < geo.K) {
-            const int64_t row0 = k * geo.G + lid0;
-            int64_t rem = geo.n - row0;
-            const int valid = rem <= 0 ? 0 : (int)(rem < nl ? rem : nl);
-            double c[NQ];
-            tile_contrib<NQ>(op, row0, valid, pbuf, c);
+          const int64_t row = (k0 + kk) * geo.G + lid0 + lane;
+          double c[NQ];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) C[(kk * NQ + q) * 32 + lane] = c[q];
-          }
+          for (int q = 0; q < NQ; ++q) c[q] = 0.0;
+          if (k0 + kk < geo.K && lane_ok && row < geo.n) row_contrib<NQ>(op, (uint32_t)row, c);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) C[(kk * NQ + q) * 32 + lane] = c[q];
         }
         __syncthreads();
-        if (warp == 0) {
-          const int kend = (int)((geo.K - k0) < B ? (geo.K - k0) : B);
-          for (int kk = 0; kk < kend; ++kk) {
+        const int kend = (int)((geo.K - k0) < B ? (geo.K - k0) : B);
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) acc[q] = add_rn(acc[q], C[(kk * NQ + q) * 32 + lane]);
+        for (int i = 0; i < QPW; ++i) {
+          const int q = warp + kWarps * i;
+          if (q < NQ) {
+            double v[B];
+#pragma unroll
+            for (int kk = 0; kk < B; ++kk) v[kk] = C[(kk * NQ + q) * 32 + lane];
+#pragma unroll
+            for (int kk = 0; kk < B; ++kk)
+              if (kk < kend) acc[i] = add_rn(acc[i], v[kk]);
           }
         }
-        __syncthreads();
       }
-      if (warp == 0 && lane < nl) {
+      if (lane_ok) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          if (q < nstore) scr.spill[(int64_t)q * geo.G + lid0 + lane] = acc[q];
+        for (int i = 0; i < QPW; ++i) {
+          const int q = warp + kWarps * i;
+          if (q < NQ && q < nstore) scr.spill[(int64_t)q * geo.G + lid0 + lane] = acc[i];
+        }
       }
-      __threadfence();
       __syncthreads();
       if (geo.gs >= 32) {
         const int g = (int)(lid0 / geo.gs);
         if (tid == 0) {
           const unsigned per = (unsigned)(geo.gs / 32);
-          unsigned t = atomicAdd(scr.gtick + g, 1u);
-          int last = (t == per - 1);
+          unsigned tk = atomic_add_release(scr.gtick + g, 1u);
+          int last = (tk == per - 1);
           if (last) scr.gtick[g] = 0u;
           s_flag = last;
         }
         __syncthreads();
         if (s_flag) {
-          __threadfence();
           group_tree<NQ>(geo, g, scr.spill, tail, part, ld, col0, nstore);
           ncomplete = 1;
         }
@@ -411,90 +376,77 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         ncomplete = g1 - g0;
       }
     } else {
-      // ---- LEAF: group g, lane thread `lane` owns lanes {lane + 32 j} ----
+      // ---- LEAF: group g; the folding lane owns lanes {lane + 32 j} ----
       const int g = (int)unit;
-      double out[NQ];
+      double out[QPW];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) out[q] = 0.0;
-      LeafStack<NQ> st{tail, 32, lane};
+      for (int i = 0; i < QPW; ++i) out[i] = 0.0;
       for (int i0 = 0; i0 < geo.m; i0 += B) {
+        double* C = Cbuf + (bpar & 1u) * (B * NQ * 32);
+        ++bpar;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int ii = warp + kWarps * u;
           const int i = i0 + ii;
-          if (i < geo.m) {
-            const int64_t row0 = (int64_t)g * geo.gs + (int64_t)brev_bits((uint32_t)i, geo.logm) * 32;
-            int64_t rem = geo.n - row0;
-            const int valid = rem <= 0 ? 0 : (int)(rem < 32 ? rem : 32);
-            double c[NQ];
-            tile_contrib<NQ>(op, row0, valid, pbuf, c);
+          const int64_t row = (int64_t)g * geo.gs + (int64_t)brev_bits((uint32_t)i, geo.logm) * 32 + lane;
+          double c[NQ];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) C[(ii * NQ + q) * 32 + lane] = c[q];
-          }
+          for (int q = 0; q < NQ; ++q) c[q] = 0.0;
+          if (i < geo.m && row < geo.n) row_contrib<NQ>(op, (uint32_t)row, c);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) C[(ii * NQ + q) * 32 + lane] = c[q];
         }
         __syncthreads();
-        if (warp == 0) {
-          const int iend = (geo.m - i0) < B ? (geo.m - i0) : B;
-          for (int ii = 0; ii < iend; ++ii) {
-            double x[NQ];
+        const int iend = (geo.m - i0) < B ? (geo.m - i0) : B;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) x[q] = C[(ii * NQ + q) * 32 + lane];
-            if (geo.m > 1) {
-              st.push((uint32_t)(i0 + ii), x, out);
-            } else {
-#pragma unroll
-              for (int q = 0; q < NQ; ++q) out[q] = x[q];
+        for (int w = 0; w < QPW; ++w) {
+          const int q = warp + kWarps * w;
+          if (q < NQ) {
+            for (int ii = 0; ii < iend; ++ii) {
+              const double x = C[(ii * NQ + q) * 32 + lane];
+              out[w] = geo.m > 1 ? leaf_push<NQ>(tail, q, lane, (uint32_t)(i0 + ii), x) : x;
             }
           }
         }
-        __syncthreads();
       }
-      if (warp == 0) {
 #pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
+      for (int w = 0; w < QPW; ++w) {
+        const int q = warp + kWarps * w;
+        if (q < NQ) {
+          double o = out[w];
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            double o = __shfl_down_sync(kFull, out[q], s);
-            if (lane < s) out[q] = add_rn(out[q], o);
+          for (int sft = 16; sft >= 1; sft >>= 1) {
+            double t = __shfl_down_sync(kFull, o, sft);
+            if (lane < sft) o = add_rn(o, t);
           }
-        }
-        if (lane == 0 && part) {
-#pragma unroll
-          for (int q = 0; q < NQ; ++q)
-            if (q < nstore) part[(int64_t)g * ld + col0 + q] = out[q];
+          if (lane == 0 && part && q < nstore) part[(int64_t)g * ld + col0 + q] = o;
         }
       }
       ncomplete = 1;
     }
     // ---- global ticket: the CTA completing the last group finalizes ----
     if (ncomplete > 0) {
-      __threadfence();
       __syncthreads();
       if (tid == 0) {
-        unsigned t = atomicAdd(ticket, (unsigned)ncomplete);
-        if (t + (unsigned)ncomplete == (unsigned)geo.n_groups) {
+        unsigned tk = atomic_add_release(ticket, (unsigned)ncomplete);
+        if (tk + (unsigned)ncomplete == (unsigned)geo.n_groups) {
           *ticket = 0u;
           s_last = 1;
-          __threadfence();
         }
       }
       __syncthreads();
     }
   }
+  __syncthreads();
   return s_last != 0;
 }
 
-// Grid-stride sweep of 32-row warp tiles (no reduction).
+// Grid-stride thread-per-row sweep (no reduction): plain SpMV / updates.
 template <class Op>
-__device__ __forceinline__ void sweep_tiles(int64_t n, const Op& op, double* smem) {
-  const int warp = threadIdx.x >> 5;
-  double* pbuf = smem + (Op::kSpmv ? warp * kPCap : 0);
-  const int64_t tiles = (n + 31) / 32;
-  const int64_t wstride = (int64_t)gridDim.x * kWarps;
-  for (int64_t t = (int64_t)blockIdx.x * kWarps + warp; t < tiles; t += wstride) {
-    const int64_t row0 = t * 32;
-    const int64_t rem = n - row0;
-    tile_apply(op, row0, (int)(rem < 32 ? rem : 32), pbuf);
+__device__ __forceinline__ void sweep_rows(int64_t n, const Op& op) {
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x) {
+    double c[1];
+    row_contrib<1>(op, (uint32_t)row, c);
   }
 }
 
