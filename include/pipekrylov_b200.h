@@ -216,6 +216,15 @@ int pk_solve_device(pk_ctx* ctx, const pk_mat* a, int32_t method, const double* 
                     void* trisolve_user, double* x_out, double* hist_out, int64_t hist_cap,
                     pk_result* result);
 
+/* ---- diagnostics (no reference counterpart) --------------------------- */
+/* Engine self-benchmark on `a` (int32 CSR): device time per launch (us) of
+ * `reps` launches of a reference kernel (kind 0: plain thread-per-row SpMV,
+ * 1: BiCGStab-shaped fused row without the ordered fold) or of the engine
+ * (2: As-SpMV with 4 ordered dots; 3, 9: engine row order without the fold;
+ * 4: grid-stride rows; 6-8: engine kernel with explicit grids).  Used by
+ * tools/dbg_simple.py to bound what the ordered fold costs. */
+int pk_debug_bench(pk_ctx* ctx, const pk_mat* a, int kind, int reps, double* us_out);
+
 #ifdef __cplusplus
 }
 #endif
