@@ -216,6 +216,17 @@ int pk_solve_device(pk_ctx* ctx, const pk_mat* a, int32_t method, const double* 
                     void* trisolve_user, double* x_out, double* hist_out, int64_t hist_cap,
                     pk_result* result);
 
+/* Transient batch (BASELINE configs[4]): nsys independent
+ * systems solved with the same method/config, each bit-identical to its own
+ * pk_solve.  mats[i] / b[i] / x0[i] (x0 nullable, or x0[i] NULL) per system,
+ * host vectors; x_out[i] / hist_out[i] host (nullable); results[nsys].
+ * `nthreads` host workers, each with its own stream, share the device of ctx.
+ * `trisolve` as for pk_solve (it may be called from several workers). */
+int pk_solve_batch(pk_ctx* ctx, int64_t nsys, const pk_mat* const* mats, int32_t method,
+                   const double* const* b, const double* const* x0, const pk_config* config,
+                   pk_trisolve_fn trisolve, void* trisolve_user, double* const* x_out,
+                   double* const* hist_out, int64_t hist_cap, pk_result* results, int32_t nthreads);
+
 /* ---- diagnostics (no reference counterpart) --------------------------- */
 /* Engine self-benchmark on `a` (int32 CSR): device time per launch (us) of
  * `reps` launches of a reference kernel (kind 0: plain thread-per-row SpMV,

@@ -42,6 +42,7 @@ from .solvers import (
     cg_pipelined,
     gmres_pipelined,
     solve,
+    solve_batch,
     solve_upper_triangular,
 )
 
@@ -53,6 +54,6 @@ __all__ = [
     "DeviceContext", "DeviceMatrix", "ExecutionContext", "ExecutionTrace", "PhaseRecord", "SolverConfig",
     "SolverResult", "UpperTriangular", "WorkgroupPartials", "as_vector", "bicgstab_pipelined",
     "cg_pipelined", "context_for", "convdiff2d", "convdiff3d", "device_matrix", "gen_poisson2d",
-    "gen_poisson3d_block", "gmres_pipelined", "poisson2d_grid", "poisson3d_grid", "solve",
+    "gen_poisson3d_block", "gmres_pipelined", "poisson2d_grid", "poisson3d_grid", "solve", "solve_batch",
     "solve_upper_triangular", "__version__",
 ]

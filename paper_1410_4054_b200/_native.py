@@ -100,6 +100,9 @@ SIGNATURES = {
                  C.POINTER(PkResult)],
     "pk_solve_device": [_P, _P, C.c_int32, _P, _P, C.POINTER(PkConfig), TRISOLVE_FN, _P, _P, _DP, C.c_int64,
                         C.POINTER(PkResult)],
+    "pk_solve_batch": [_P, C.c_int64, C.POINTER(_P), C.c_int32, C.POINTER(_P), C.POINTER(_P),
+                       C.POINTER(PkConfig), TRISOLVE_FN, _P, C.POINTER(_P), C.POINTER(_P), C.c_int64,
+                       C.POINTER(PkResult), C.c_int32],
     "pk_debug_bench": [_P, _P, C.c_int, C.c_int, _DP],
 }
 _RESTYPES = {"pk_last_error": C.c_char_p}

@@ -337,3 +337,58 @@ def solve_resident(method: str, a, b, x0=None, config=None, context=None, profil
                      "kernel_seconds": [float(v) for v in res.kernel_seconds],
                      "kernel_launches": [int(v) for v in res.kernel_launches]})
     return x, result
+
+
+def solve_batch(systems, tag=("cg", "pipelined"), config=None, context=None, threads: int = 16):
+    """Transient batch (BASELINE configs[4]): independent systems ``[(A, b)]``
+    or ``[(A, b, x0)]`` solved with the same driver and config, no
+    communication.  ``threads`` host workers (each with its own CUDA stream)
+    overlap the device-resident solves; every result is bit-identical to
+    ``SOLVERS[tag](A, b, x0, config, context)`` on its own.  Matrices are
+    uploaded once per object.  Returns a list of :class:`SolverResult`."""
+    if isinstance(tag, str):
+        tag = (tag, "pipelined")
+    if tuple(tag) not in SOLVERS:
+        raise ValueError(f"unknown solver {tag!r}; the B200 path implements {sorted(SOLVERS)}")
+    method = tag[0]
+    cfg = SolverConfig.coerce(config)
+    if method == "gmres" and cfg.orthogonalization != CLASSICAL_GS:
+        raise ValueError("pipelined GMRES supports classical Gram-Schmidt only")
+    ctx = ExecutionContext.coerce(context)
+    dc = context_for(ctx)
+    systems = list(systems)
+    nsys = len(systems)
+    mats, bs, x0s, xs, hists = [], [], [], [], []
+    limit = cfg.iteration_limit()
+    for item in systems:
+        a, b = item[0], item[1]
+        x0 = item[2] if len(item) > 2 else None
+        a, b, x0 = _prepare(a, b, x0)
+        dm = device_matrix(a, ctx)
+        mats.append(dm)
+        bs.append(b)
+        x0s.append(x0)
+        xs.append(np.empty(dm.n_rows))
+        hists.append(np.empty(max(limit, 1)))
+    P = C.c_void_p
+    dp = lambda v: C.cast(v.ctypes.data, P) if v is not None else None
+    mat_arr = (P * max(nsys, 1))(*[m.handle for m in mats])
+    b_arr = (P * max(nsys, 1))(*[dp(v) for v in bs])
+    x0_arr = (P * max(nsys, 1))(*[dp(v) for v in x0s])
+    x_arr = (P * max(nsys, 1))(*[dp(v) for v in xs])
+    h_arr = (P * max(nsys, 1))(*[dp(v) for v in hists])
+    res = (N.PkResult * max(nsys, 1))()
+    ncfg = _native_config(cfg)
+    dc.reset_stream()
+    N.check(N.lib().pk_solve_batch(dc.handle, nsys, mat_arr, N.METHODS[method], b_arr, x0_arr, C.byref(ncfg),
+                                   _trisolve_cb, None, x_arr, h_arr, max(limit, 1), res, int(threads)),
+            f"{method}_pipelined batch")
+    out = []
+    for i in range(nsys):
+        r = res[i]
+        out.append(SolverResult(
+            x=xs[i], residual_history=[float(v) for v in hists[i][: r.iterations]],
+            true_final_residual=float(r.true_final_residual), iterations=int(r.iterations),
+            termination=N.TERM_NAMES[r.termination], trace=_trace_from(r, method, mats[i].n_rows, cfg.restart),
+            breakdown_kind=N.KIND_NAMES[r.breakdown_kind], loop_seconds=float(r.loop_seconds), diagnostics={}))
+    return out

@@ -207,3 +207,35 @@ def test_c3_gmres_128_fixed_bitwise(pk):
     cfg = pk.SolverConfig(fixed_iterations=6, max_iterations=6)
     res = pk.gmres_pipelined(dm, b, config=cfg)
     assert_identical(res, oracle_run("gmres", a, b, (128, 256), fixed=6, max_iterations=6))
+
+
+# ---------------------------------------------------------------------------
+# C5: transient batch of independent systems
+# ---------------------------------------------------------------------------
+
+
+def test_c5_batch_each_system_bitwise(pk):
+    """configs[4] in miniature: mixed sizes, distinct seeded RHS; every system
+    of the batch equals its own single solve and the oracle, bitwise."""
+    sides = [15, 31, 63, 31, 15, 47, 63, 15]
+    mats = {s: pk.poisson2d_grid(s)[0] for s in set(sides)}
+    systems = [(mats[s], np.random.default_rng(i).random(s * s)) for i, s in enumerate(sides)]
+    ctx = pk.ExecutionContext(4, 64)
+    out = pk.solve_batch(systems, tag="cg", config=pk.SolverConfig(max_iterations=400), context=ctx, threads=3)
+    assert len(out) == len(systems)
+    for i, ((a, b), r) in enumerate(zip(systems, out)):
+        single = pk.cg_pipelined(a, b, config=pk.SolverConfig(max_iterations=400), context=ctx)
+        assert r.iterations == single.iterations and same(r.x, single.x)
+        assert same(r.residual_history, single.residual_history)
+        if i < 3:
+            assert_identical(r, oracle_run("cg", a, b, (4, 64), max_iterations=400))
+
+
+@pytest.mark.parametrize("tag", ["bicgstab", "gmres"])
+def test_batch_other_drivers(pk, tag):
+    a, b = pk.convdiff2d(24)
+    systems = [(a, b * (1.0 + k)) for k in range(4)]
+    out = pk.solve_batch(systems, tag=tag, config=pk.SolverConfig(max_iterations=300), threads=2)
+    for (aa, bb), r in zip(systems, out):
+        single = pk.SOLVERS[(tag, "pipelined")](aa, bb, config=pk.SolverConfig(max_iterations=300))
+        assert r.iterations == single.iterations and same(r.x, single.x)
