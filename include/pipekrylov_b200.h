@@ -76,6 +76,7 @@ extern "C" {
 
 typedef struct pk_ctx pk_ctx; /* device + stream + reduction geometry */
 typedef struct pk_mat pk_mat; /* device-resident CSR matrix           */
+typedef struct pk_dcg pk_dcg; /* row-partitioned CG solver (C4)       */
 
 /* SolverConfig (solvers.py:104-145).  fixed_iterations <= 0 means None. */
 typedef struct pk_config {
@@ -149,6 +150,12 @@ int pk_csr_upload(pk_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* ro
  * io.py:201-275 and the convection-diffusion families). */
 int pk_csr_generate(pk_ctx* ctx, int32_t family, const int64_t* dims, int32_t ndims,
                     const double* coef, int32_t ncoef, pk_mat** out);
+/* Rows [row_lo, row_hi) of a generator family with columns stored as
+ * (global column - col_base) and n_cols_local columns: the local block of a
+ * row partition with halo. */
+int pk_csr_generate_rows(pk_ctx* ctx, int32_t family, const int64_t* dims, int32_t ndims,
+                         const double* coef, int32_t ncoef, int64_t row_lo, int64_t row_hi,
+                         int64_t col_base, int64_t n_cols_local, pk_mat** out);
 int pk_csr_info(const pk_mat* mat, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
                 int64_t* max_row_nnz);
 /* Copy the CSR arrays back to host (generator-equality tests). */
@@ -226,6 +233,25 @@ int pk_solve_batch(pk_ctx* ctx, int64_t nsys, const pk_mat* const* mats, int32_t
                    const double* const* b, const double* const* x0, const pk_config* config,
                    pk_trisolve_fn trisolve, void* trisolve_user, double* const* x_out,
                    double* const* hist_out, int64_t hist_cap, pk_result* results, int32_t nthreads);
+
+/* ---- row-partitioned CG (BASELINE configs[3]) -------- */
+/* gen_poisson3d_block(side, 1) split into `world` group-aligned z-slabs; per
+ * iteration one halo exchange (r, p, Ap; one plane per neighbour), the fused
+ * CG kernel on the local rows, ONE allgather of the group partials and the
+ * same serial stage 2 on every rank: bit-identical to cg_pipelined on one
+ * device at the geometry n_groups x group_size (which must equal n).
+ * comm NULL: all `world` partitions inside this process on ctx's device
+ * (halo = device copies); otherwise an ncclComm_t from pk_nccl_comm_create
+ * and this process owns partition `rank`.  b: host right-hand side (global
+ * for comm NULL, the own rows otherwise; NULL = ones); x_out likewise. */
+int pk_nccl_unique_id(void* out /* 128 bytes */);
+int pk_nccl_comm_create(int device, const void* unique_id, int nranks, int rank, void** comm);
+int pk_nccl_comm_destroy(void* comm);
+int pk_dcg_create(pk_ctx* ctx, int64_t side, int64_t n_groups, int64_t group_size, int32_t world,
+                  int32_t rank, void* comm, int64_t hist_cap, pk_dcg** out);
+int pk_dcg_solve(pk_dcg* dcg, const double* b, const pk_config* config, double* x_out, double* hist_out,
+                 int64_t hist_cap, pk_result* result);
+int pk_dcg_destroy(pk_dcg* dcg);
 
 /* ---- diagnostics (no reference counterpart) --------------------------- */
 /* Engine self-benchmark on `a` (int32 CSR): device time per launch (us) of

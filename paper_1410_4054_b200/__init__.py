@@ -16,6 +16,7 @@ from .generators import (
     poisson2d_grid,
     poisson3d_grid,
 )
+from .partition import PartitionedCG, cg_partitioned, slab_geometry
 from .linalg import (
     DEFAULT_CONTEXT,
     CsrMatrix,
@@ -50,10 +51,10 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BREAKDOWN", "CLASSICAL_GS", "CONVERGED", "DEFAULT_BREAKDOWN_TOLERANCE", "DEFAULT_CONTEXT",
-    "LUCKY_BREAKDOWN", "MAX_ITER", "MODIFIED_GS", "SOLVERS", "BreakdownError", "CsrMatrix",
+    "LUCKY_BREAKDOWN", "MAX_ITER", "MODIFIED_GS", "PartitionedCG", "SOLVERS", "BreakdownError", "CsrMatrix",
     "DeviceContext", "DeviceMatrix", "ExecutionContext", "ExecutionTrace", "PhaseRecord", "SolverConfig",
     "SolverResult", "UpperTriangular", "WorkgroupPartials", "as_vector", "bicgstab_pipelined",
-    "cg_pipelined", "context_for", "convdiff2d", "convdiff3d", "device_matrix", "gen_poisson2d",
+    "cg_partitioned", "cg_pipelined", "context_for", "convdiff2d", "convdiff3d", "device_matrix", "gen_poisson2d",
     "gen_poisson3d_block", "gmres_pipelined", "poisson2d_grid", "poisson3d_grid", "solve", "solve_batch",
-    "solve_upper_triangular", "__version__",
+    "slab_geometry", "solve_upper_triangular", "__version__",
 ]

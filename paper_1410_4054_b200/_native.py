@@ -103,6 +103,14 @@ SIGNATURES = {
     "pk_solve_batch": [_P, C.c_int64, C.POINTER(_P), C.c_int32, C.POINTER(_P), C.POINTER(_P),
                        C.POINTER(PkConfig), TRISOLVE_FN, _P, C.POINTER(_P), C.POINTER(_P), C.c_int64,
                        C.POINTER(PkResult), C.c_int32],
+    "pk_csr_generate_rows": [_P, C.c_int32, _I64P, C.c_int32, _DP, C.c_int32, C.c_int64, C.c_int64, C.c_int64,
+                             C.c_int64, C.POINTER(_P)],
+    "pk_nccl_unique_id": [_P],
+    "pk_nccl_comm_create": [C.c_int, _P, C.c_int, C.c_int, C.POINTER(_P)],
+    "pk_nccl_comm_destroy": [_P],
+    "pk_dcg_create": [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _P, C.c_int64, C.POINTER(_P)],
+    "pk_dcg_solve": [_P, _DP, C.POINTER(PkConfig), _DP, _DP, C.c_int64, C.POINTER(PkResult)],
+    "pk_dcg_destroy": [_P],
     "pk_debug_bench": [_P, _P, C.c_int, C.c_int, _DP],
 }
 _RESTYPES = {"pk_last_error": C.c_char_p}

@@ -180,6 +180,8 @@ __global__ void k_fill_i32(int32_t* p, int32_t v) { *p = v; }
 // ---------------------------------------------------------------------------
 
 struct StencilSpec {
+  int64_t row_lo;     // first global row generated (local row i = global row_lo + i)
+  int64_t col_base;   // stored column = global column - col_base
   int32_t nent;
   int64_t off[8];     // column offset, sorted ascending
   int32_t axis[8];    // -1 for the diagonal
@@ -200,7 +202,7 @@ __device__ __forceinline__ bool stencil_valid(const StencilSpec& s, int64_t row,
 __global__ void k_gen_count(int64_t n, StencilSpec s, int64_t* counts) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int c = 0;
-    for (int e = 0; e < s.nent; ++e) c += stencil_valid(s, i, e);
+    for (int e = 0; e < s.nent; ++e) c += stencil_valid(s, s.row_lo + i, e);
     counts[i] = c;
   }
 }
@@ -209,9 +211,10 @@ template <typename RowT>
 __global__ void k_gen_fill(int64_t n, StencilSpec s, const RowT* rowptr, int32_t* cols, double* vals) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     RowT k = rowptr[i];
+    const int64_t gi = s.row_lo + i;
     for (int e = 0; e < s.nent; ++e) {
-      if (stencil_valid(s, i, e)) {
-        cols[k] = (int32_t)(i + s.off[e]);
+      if (stencil_valid(s, gi, e)) {
+        cols[k] = (int32_t)(gi + s.off[e] - s.col_base);
         vals[k] = s.val[e];
         ++k;
       }
@@ -656,8 +659,27 @@ extern "C" int pk_csr_upload(pk_ctx* c, int64_t n_rows, int64_t n_cols, const in
   return PK_OK;
 }
 
+static int gen_stencil(pk_ctx* c, int32_t family, const int64_t* dims, int32_t ndims, const double* coef,
+                       int32_t ncoef, int64_t row_lo, int64_t row_hi, int64_t col_base, int64_t n_cols_local,
+                       pk_mat** out);
+
 extern "C" int pk_csr_generate(pk_ctx* c, int32_t family, const int64_t* dims, int32_t ndims, const double* coef,
                                int32_t ncoef, pk_mat** out) {
+  return gen_stencil(c, family, dims, ndims, coef, ncoef, 0, -1, 0, -1, out);
+}
+
+extern "C" int pk_csr_generate_rows(pk_ctx* c, int32_t family, const int64_t* dims, int32_t ndims,
+                                    const double* coef, int32_t ncoef, int64_t row_lo, int64_t row_hi,
+                                    int64_t col_base, int64_t n_cols_local, pk_mat** out) {
+  if (row_lo < 0 || row_hi < row_lo) return fail(PK_ERR_INVALID, "bad row range");
+  return gen_stencil(c, family, dims, ndims, coef, ncoef, row_lo, row_hi, col_base, n_cols_local, out);
+}
+
+// Rows [row_lo, row_hi) of a stencil family (row_hi < 0: all rows), columns
+// stored as global - col_base, matrix n_cols = n_cols_local (< 0: n).
+static int gen_stencil(pk_ctx* c, int32_t family, const int64_t* dims, int32_t ndims, const double* coef,
+                       int32_t ncoef, int64_t row_lo, int64_t row_hi, int64_t col_base, int64_t n_cols_local,
+                       pk_mat** out) {
   if (!c || !out || !dims) return fail(PK_ERR_INVALID, "NULL argument");
   *out = nullptr;
   StencilSpec sp{};
@@ -672,6 +694,13 @@ extern "C" int pk_csr_generate(pk_ctx* c, int32_t family, const int64_t* dims, i
     n *= dims[d];
   }
   if (n >= (1ll << 31) - 1) return fail(PK_ERR_UNSUPPORTED, "grid too large for int32 row indices");
+  if (row_hi < 0) row_hi = n;
+  if (row_hi > n || row_lo > row_hi) return fail(PK_ERR_INVALID, "row range outside the grid");
+  const int64_t n_global = n;
+  const int64_t ncols = n_cols_local < 0 ? n_global : n_cols_local;
+  sp.row_lo = row_lo;
+  sp.col_base = col_base;
+  n = row_hi - row_lo;  // rows generated
   // per-direction values: {axis, step, value}
   double diag = 0.0;
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
@@ -733,7 +762,7 @@ extern "C" int pk_csr_generate(pk_ctx* c, int32_t family, const int64_t* dims, i
   PK_CUDA(cudaMemcpyAsync(bsum_incl, hb.data(), nblk * 8, cudaMemcpyHostToDevice, s));
   k_scan_add<<<(unsigned)nblk, 1024, 0, s>>>(incl, n, bsum_incl);
   pk_mat* m = nullptr;
-  int rc = alloc_mat(c, n, n, nnz, &m);
+  int rc = alloc_mat(c, n, ncols, nnz, &m);
   if (rc == PK_OK) {
     m->max_row = (int64_t)hmax;
     if (m->row64) {
@@ -939,6 +968,7 @@ extern "C" int pk_gs_normalize(pk_ctx* c, int64_t n, double* v, const double* no
 }
 
 #include "pk_solvers.inc"
+#include "pk_dist.inc"
 
 // ---------------------------------------------------------------------------
 // engine experiments (not part of the public header): simple reference

@@ -300,10 +300,11 @@ struct OpSpmvFused {
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
   Csr<RowT> A;
-  const double* __restrict__ p;
+  const double* __restrict__ p;  // gather base (column index space)
   double* q;
   int32_t kind[4];
   const double* w[4];
+  int64_t own_off;                // own row i of p is p[own_off + i] (row-partitioned halo layout)
   struct Item { double pv; double wv[NQ > 0 ? NQ : 1]; };
   struct Gat { double v; };
   __device__ __forceinline__ void load(uint32_t row, Item& it) const {
@@ -311,7 +312,7 @@ struct OpSpmvFused {
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
       it.wv[k] = 0.0;
-      if (kind[k] == PK_DOT_INPUT) it.pv = __ldg(p + row);
+      if (kind[k] == PK_DOT_INPUT) it.pv = __ldg(p + own_off + row);
       if (kind[k] == PK_DOT_VECTOR) it.wv[k] = __ldg(w[k] + row);
     }
   }
@@ -376,9 +377,13 @@ struct OpCgFused {
   double* p[2];
   double* ap[2];
   double alpha, beta;
-  const double* rc;  // current halves, resolved in scalars()
+  int64_t goff;      // gather base = own base - goff (row-partitioned halo layout; 0 otherwise)
+  const double* rc;  // current halves (own rows), resolved in scalars()
   const double* pc;
   const double* apc;
+  const double* rg;  // the same vectors in column index space
+  const double* pg;
+  const double* apg;
   double* rn_;
   double* pn_;
   double* apn_;
@@ -388,7 +393,7 @@ struct OpCgFused {
     it.x = __ldg(x + row); it.r = __ldg(rc + row); it.p = __ldg(pc + row); it.ap = __ldg(apc + row);
   }
   __device__ __forceinline__ void gload(uint32_t col, Gat& g) const {
-    g.r = __ldg(rc + col); g.ap = __ldg(apc + col); g.p = __ldg(pc + col);
+    g.r = __ldg(rg + col); g.ap = __ldg(apg + col); g.p = __ldg(pg + col);
   }
   __device__ __forceinline__ double gval(const Gat& g) const {
     double rn = sub_rn(g.r, mul_rn(alpha, g.ap));
@@ -410,6 +415,7 @@ struct OpCgFused {
     const int cur = ld_par(sp.par);
     rc = cur ? r[1] : r[0]; pc = cur ? p[1] : p[0]; apc = cur ? ap[1] : ap[0];
     rn_ = cur ? r[0] : r[1]; pn_ = cur ? p[0] : p[1]; apn_ = cur ? ap[0] : ap[1];
+    rg = rc - goff; pg = pc - goff; apg = apc - goff;
   }
 };
 

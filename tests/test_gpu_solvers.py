@@ -239,3 +239,32 @@ def test_batch_other_drivers(pk, tag):
     for (aa, bb), r in zip(systems, out):
         single = pk.SOLVERS[(tag, "pipelined")](aa, bb, config=pk.SolverConfig(max_iterations=300))
         assert r.iterations == single.iterations and same(r.x, single.x)
+
+
+# ---------------------------------------------------------------------------
+# C4: row-partitioned CG (in-process partitions on one device)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_c4_partitioned_cg_bitwise(pk, world):
+    """gen_poisson3d_block(32, 1) split into `world` z-slabs: halo exchange +
+    one partials allgather per iteration reproduce the single-device oracle at
+    the same geometry bit for bit."""
+    side, gs = 32, 1024
+    geom = pk.slab_geometry(side, gs)
+    a, b = pk.gen_poisson3d_block(side, 1)
+    res = pk.cg_partitioned(side, world, gs, config=pk.SolverConfig(max_iterations=400))
+    assert_identical(res, oracle_run("cg", a, b, (geom.n_groups, geom.group_size), max_iterations=400))
+
+
+def test_c4_partitioned_random_rhs_fixed_iterations(pk):
+    side, gs = 16, 512
+    geom = pk.slab_geometry(side, gs)
+    a, _ = pk.gen_poisson3d_block(side, 1)
+    b = np.random.default_rng(3).random(side ** 3)
+    cfg = pk.SolverConfig(fixed_iterations=25, max_iterations=25)
+    res = pk.cg_partitioned(side, 4, gs, b=b, config=cfg)
+    assert_identical(res, oracle_run("cg", a, b, (geom.n_groups, geom.group_size), fixed=25, max_iterations=25))
+    single = pk.cg_pipelined(a, b, config=cfg, context=geom)
+    assert same(single.x, res.x) and same(single.residual_history, res.residual_history)
