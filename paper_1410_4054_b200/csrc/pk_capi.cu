@@ -105,6 +105,23 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (last && fin != FIN_NONE && st && threadIdx.x < 32) finalize(st, fin, fin_arg, ing);  // warp 0 of the last CTA
 }
 
+// One warp per CTA, one unit per warp (CHAIN mapping with group_size >= 32).
+template <int NQ, int R, class Op>
+__global__ void __launch_bounds__(32, 8)
+    k_reduce_warp(const __grid_constant__ Geom geo, const __grid_constant__ Op op0, ScalarPtrs sp, double* part,
+                  int ld, int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin,
+                  int fin_arg) {
+  extern __shared__ double smem[];
+  if (skip && *(volatile const int32_t*)skip) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  if (st && !gate_open(st, gate, ing)) return;
+  Op op = op0;
+  op.scalars(sp);
+  bool last = engine_warp_chain<NQ, R>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+  if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing);
+}
+
 template <class Op>
 __global__ void __launch_bounds__(256, 4) k_sweep(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
   if (st && !gate_open(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0)) return;
@@ -260,7 +277,9 @@ __global__ void k_row_max(const int64_t* counts, int64_t n, unsigned long long* 
   unsigned long long m = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     m = max(m, (unsigned long long)counts[i]);
-  atomicMax(mx, m);
+  // warp maximum first: one atomic per warp instead of one per thread
+  for (int s = 16; s >= 1; s >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, s));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
 }
 
 // ---------------------------------------------------------------------------
@@ -305,6 +324,11 @@ struct RowsPerThread { static constexpr int value = 2; };
 template <class Op>
 struct RowsPerThread<Op, std::void_t<decltype(Op::kRowsPerThread)>> { static constexpr int value = Op::kRowsPerThread; };
 
+template <class Op, class = void>
+struct WarpRows { static constexpr int value = 4; };
+template <class Op>
+struct WarpRows<Op, std::void_t<decltype(Op::kWarpRows)>> { static constexpr int value = Op::kWarpRows; };
+
 template <int NQ, class Op, int U = (NQ <= 4 ? RowsPerThread<Op>::value : 1)>
 static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp,
                          double* part, int ld, int col0, SolveState* st = nullptr, int gate = GATE_NONE,
@@ -313,6 +337,22 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
   Geom geo = make_geom(n, c->ng, c->gs);
   if (!geo.leaf && (size_t)geo.G * (size_t)nstore > c->spill_cap)
     return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
+  if constexpr (NQ <= 4) {
+  if (!geo.leaf && geo.gs >= 32 && geo.K >= 2 && geo.K <= 8) {
+    // warp-per-unit chain engine (no shared staging, no CTA barrier): wins
+    // for short chains (small, latency-bound systems, e.g. CG 512^2: 20.6 vs
+    // 26.8 us/iter); long chains keep the CTA engine (C2: 44.7 vs 63.8 us)
+    constexpr int R = WarpRows<Op>::value;
+    const size_t wsm = warp_chain_smem_bytes(geo, NQ);
+    auto kw = k_reduce_warp<NQ, R, Op>;
+    if (wsm + 1024 > 48 * 1024) PK_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    kw<<<(unsigned)geo.units, 32, wsm, s>>>(geo, op, sp, part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin,
+                                            fin_arg);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("warp engine launch: ") + cudaGetErrorString(e));
+    return PK_OK;
+  }
+  }
   size_t smem = engine_smem_bytes(geo, NQ, U);
   constexpr int MINB = NQ > 8 ? 1 : (NQ > 4 ? 2 : Op::kMinBlocks);
   auto kern = k_reduce<NQ, U, MINB, Op>;

@@ -472,6 +472,7 @@ struct OpBicgA {
   static constexpr int kMinBlocks = 2;
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
+  static constexpr int kWarpRows = 2;
   Csr<RowT> A;
   double* x;
   double* r[2];
@@ -673,6 +674,7 @@ template <int NB>
 struct OpMultiDot {
   static constexpr bool kSpmv = false;
   static constexpr int kMinBlocks = 4;
+  static constexpr int kWarpRows = NB > 8 ? 1 : 2;
   const double* __restrict__ v;
   int32_t nb;
   const double* b[NB];
@@ -698,6 +700,7 @@ template <int NB>
 struct OpGsUpdate {
   static constexpr bool kSpmv = false;
   static constexpr int kMinBlocks = NB > 8 ? 2 : 4;
+  static constexpr int kWarpRows = NB > 8 ? 1 : 2;
   double* v;
   int32_t nb;
   const double* b[NB];

@@ -36,6 +36,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace pk {
 
 constexpr int kWarps = 8;  // warps of an engine CTA
@@ -135,14 +137,24 @@ struct Csr {
 // (_spmvkernels.py:12-18).  kSlots entries per pass: all loads of a pass are
 // issued first (slots past the row end re-read its last entry -- always a
 // valid address -- and are not added), then the ordered adds.
+template <class Op, class = void>
+struct RowBounds { using T = int32_t; };
+template <class Op>
+struct RowBounds<Op, std::void_t<typename Op::RowT>> { using T = typename Op::RowT; };
+
+// rb_pre/re_pre: the row's CSR bounds when already loaded (software
+// pipelining across batches), else rb_pre > re_pre (load them here)
 template <int NQ, class Op>
-__device__ __forceinline__ void row_contrib(const Op& op, uint32_t row, double (&c)[NQ]) {
+__device__ __forceinline__ void row_contrib(const Op& op, uint32_t row, double (&c)[NQ],
+                                            typename RowBounds<Op>::T rb_pre = 1,
+                                            typename RowBounds<Op>::T re_pre = 0) {
   typename Op::Item it;
   op.load(row, it);
   if constexpr (Op::kSpmv) {
     using RowT = typename Op::RowT;
     constexpr int S = Op::kSlots;
-    const RowT b = __ldg(op.A.rp + row), e = __ldg(op.A.rp + row + 1);
+    const bool have = rb_pre <= re_pre;
+    const RowT b = have ? rb_pre : __ldg(op.A.rp + row), e = have ? re_pre : __ldg(op.A.rp + row + 1);
     double acc = 0.0;
     for (RowT k0 = b; k0 < e; k0 += S) {
       int32_t col[S];
@@ -317,6 +329,10 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
       double acc[QPW];
 #pragma unroll
       for (int i = 0; i < QPW; ++i) acc[i] = 0.0;
+      using RB = typename RowBounds<Op>::T;
+      RB nb[U], ne[U];  // CSR bounds of this warp's rows in the next batch
+#pragma unroll
+      for (int u = 0; u < U; ++u) { nb[u] = 1; ne[u] = 0; }
       for (int64_t k0 = 0; k0 < geo.K; k0 += B) {
         double* C = Cbuf + (bpar & 1u) * (B * NQ * 32);
         ++bpar;
@@ -327,9 +343,24 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
           double c[NQ];
 #pragma unroll
           for (int q = 0; q < NQ; ++q) c[q] = 0.0;
-          if (k0 + kk < geo.K && lane_ok && row < geo.n) row_contrib<NQ>(op, (uint32_t)row, c);
+          if (k0 + kk < geo.K && lane_ok && row < geo.n) row_contrib<NQ>(op, (uint32_t)row, c, nb[u], ne[u]);
 #pragma unroll
           for (int q = 0; q < NQ; ++q) C[(kk * NQ + q) * 32 + lane] = c[q];
+        }
+        if constexpr (Op::kSpmv) {
+          // software pipelining: the next batch's row bounds load during the
+          // barrier and the fold (one dependent DRAM round trip less per row)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t kn = k0 + B + warp + kWarps * u;
+            const int64_t rn = kn * geo.G + lid0 + lane;
+            nb[u] = 1;
+            ne[u] = 0;
+            if (kn < geo.K && lane_ok && rn < geo.n) {
+              nb[u] = __ldg(op.A.rp + rn);
+              ne[u] = __ldg(op.A.rp + rn + 1);
+            }
+          }
         }
         __syncthreads();
         const int kend = (int)((geo.K - k0) < B ? (geo.K - k0) : B);
@@ -439,6 +470,188 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
   }
   __syncthreads();
   return s_last != 0;
+}
+
+// Warp-level halving tree of group g over its gs (>= 32) spilled lane values:
+// lane l owns the lanes {l + 32 j}, visited in bit-reversed order of j
+// through a binary-counter stack (stk: (log2(gs/32)+1) x NQ x 32 doubles),
+// then a shuffle tree across the 32 lanes.
+template <int NQ>
+__device__ __forceinline__ void group_tree_warp(const Geom& geo, int g, const double* spill, double* stk,
+                                                double* part, int ld, int col0, int nstore) {
+  const int lane = threadIdx.x & 31;
+  double v[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = 0.0;
+  const int64_t base = (int64_t)g * geo.gs;
+  const int mm = geo.gs / 32;
+  const int lg = ilog2_u((uint32_t)mm);
+  LeafStack<NQ> st{stk, 32, lane};
+  for (int i = 0; i < mm; ++i) {
+    const int64_t idx = base + (int64_t)brev_bits((uint32_t)i, lg) * 32 + lane;
+    double x[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) x[q] = q < nstore ? __ldcg(spill + (int64_t)q * geo.G + idx) : 0.0;
+    if (mm > 1) {
+      st.push((uint32_t)i, x, v);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) v[q] = x[q];
+    }
+  }
+#pragma unroll
+  for (int sft = 16; sft >= 1; sft >>= 1) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double o = __shfl_down_sync(kFull, v[q], sft);
+      if (lane < sft) v[q] = add_rn(v[q], o);
+    }
+  }
+  if (lane == 0 && part) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (q < nstore) part[(int64_t)g * ld + col0 + q] = v[q];
+  }
+  __syncwarp();
+}
+
+inline size_t warp_chain_smem_bytes(const Geom& g, int nq) {
+  return (size_t)(ilog2_u((uint32_t)(g.gs / 32)) + 1) * nq * 32 * sizeof(double);
+}
+
+// ---------------------------------------------------------------------------
+// warp-per-unit CHAIN engine (no shared memory, no CTA barrier)
+// ---------------------------------------------------------------------------
+//
+// R rows of one lane chain, computed with interleaved loads (R independent
+// row chains in flight per thread): contributions c[r][q] of rows
+// (k0 + r) G + lid0 + lane, r < R; rows outside the matrix contribute 0.
+template <int NQ, int R, class Op>
+__device__ __forceinline__ void rows_contrib(const Op& op, const Geom& geo, int64_t k0, int64_t lid0, bool lane_ok,
+                                             double (&c)[R][NQ]) {
+  const int lane = threadIdx.x & 31;
+  bool ok[R];
+  uint32_t row[R];
+  typename Op::Item it[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t rw = (k0 + r) * geo.G + lid0 + lane;
+    ok[r] = lane_ok && (k0 + r) < geo.K && rw < geo.n;
+    row[r] = ok[r] ? (uint32_t)rw : 0u;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) c[r][q] = 0.0;
+  }
+  if constexpr (Op::kSpmv) {
+    using RowT = typename Op::RowT;
+    constexpr int S = Op::kSlots;
+    RowT b[R], e[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      b[r] = ok[r] ? __ldg(op.A.rp + row[r]) : (RowT)0;
+      e[r] = ok[r] ? __ldg(op.A.rp + row[r] + 1) : (RowT)0;
+      if (ok[r]) op.load(row[r], it[r]);
+    }
+    // first S entries of every row: all loads in flight, then the ordered adds
+    int32_t col[R][S];
+    double val[R][S];
+    typename Op::Gat gv[R][S];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        const RowT k = (b[r] + j < e[r]) ? b[r] + j : (e[r] > b[r] ? e[r] - 1 : b[r]);
+        const bool live = e[r] > b[r];
+        col[r][j] = live ? __ldg(op.A.ci + k) : 0;
+        val[r][j] = live ? __ldg(op.A.va + k) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int j = 0; j < S; ++j) op.gload((uint32_t)col[r][j], gv[r][j]);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        if (b[r] + j < e[r]) acc = add_rn(acc, mul_rn(val[r][j], op.gval(gv[r][j])));
+      // rows longer than S: the rest in order, straight from memory
+      for (RowT k = b[r] + S; k < e[r]; ++k) {
+        typename Op::Gat g;
+        op.gload((uint32_t)__ldg(op.A.ci + k), g);
+        acc = add_rn(acc, mul_rn(__ldg(op.A.va + k), op.gval(g)));
+      }
+      if (ok[r]) op.compute(row[r], it[r], acc, c[r]);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (ok[r]) op.load(row[r], it[r]);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (ok[r]) op.compute(row[r], it[r], c[r]);
+  }
+}
+
+// One warp per unit of 32 lane ids (CHAIN mapping, group_size >= 32): the warp
+// walks the unit's K chunks R at a time and folds each lane's chain in
+// registers in the reference order; the warp that completes a group runs the
+// group's halving tree (warp-level); the warp completing the last group is
+// the finalizer.  Returns true in that warp.
+template <int NQ, int R, class Op>
+__device__ __forceinline__ bool engine_warp_chain(const Geom& geo, const Op& op, double* stk, double* part, int ld,
+                                                  int col0, int nstore, const Scratch& scr, unsigned* ticket) {
+  const int lane = threadIdx.x & 31;
+  const int wpc = blockDim.x >> 5;
+  const int64_t w0 = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * wpc;
+  bool last = false;
+  for (int64_t unit = w0; unit < geo.units; unit += nw) {
+    const int64_t lid0 = unit * 32;
+    const int nl = (int)((geo.G - lid0) < 32 ? (geo.G - lid0) : 32);
+    const bool lane_ok = lane < nl;
+    double acc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+    for (int64_t k0 = 0; k0 < geo.K; k0 += R) {
+      double c[R][NQ];
+      rows_contrib<NQ, R>(op, geo, k0, lid0, lane_ok, c);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (k0 + r < geo.K) {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) acc[q] = add_rn(acc[q], c[r][q]);
+        }
+    }
+    if (lane_ok) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < nstore) scr.spill[(int64_t)q * geo.G + lid0 + lane] = acc[q];
+    }
+    __syncwarp();
+    const int g = (int)(lid0 / geo.gs);
+    int lastg = 0;
+    if (lane == 0) {
+      const unsigned per = (unsigned)(geo.gs / 32);
+      unsigned tk = atomic_add_release(scr.gtick + g, 1u);
+      lastg = (tk == per - 1);
+      if (lastg) scr.gtick[g] = 0u;
+    }
+    lastg = __shfl_sync(kFull, lastg, 0);
+    if (lastg) {
+      group_tree_warp<NQ>(geo, g, scr.spill, stk, part, ld, col0, nstore);
+      int l = 0;
+      if (lane == 0) {
+        unsigned tk = atomic_add_release(ticket, 1u);
+        if (tk + 1u == (unsigned)geo.n_groups) {
+          *ticket = 0u;
+          l = 1;
+        }
+      }
+      if (__shfl_sync(kFull, l, 0)) last = true;
+    }
+  }
+  return last;
 }
 
 // Grid-stride thread-per-row sweep (no reduction): plain SpMV / updates.
