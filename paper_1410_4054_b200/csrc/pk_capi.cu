@@ -288,10 +288,12 @@ __global__ void k_row_max(const int64_t* counts, int64_t n, unsigned long long* 
 
 // Scratch of the engine (CHAIN spill + per-group tickets), sized for nq
 // quantities.  Must be called outside stream capture (it may reallocate).
+static int64_t min_units(const pk_ctx* c) { return (int64_t)c->sm_count * 4; }
+
 static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
-  Geom geo = make_geom(n, c->ng, c->gs);
-  if (geo.leaf) return PK_OK;
-  size_t need = (size_t)geo.G * (size_t)std::max(nq, 1);
+  Geom geo = make_geom(n, c->ng, c->gs, min_units(c));
+  if (geo.leaf && geo.logf == 0) return PK_OK;
+  size_t need = geo.leaf ? (size_t)geo.units * 32 * (size_t)std::max(nq, 1) : (size_t)geo.G * (size_t)std::max(nq, 1);
   if (need <= c->spill_cap) return PK_OK;
   PK_CUDA(cudaStreamSynchronize(c->stream));
   if (c->spill) cudaFree(c->spill);
@@ -334,8 +336,10 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
                          double* part, int ld, int col0, SolveState* st = nullptr, int gate = GATE_NONE,
                          const int32_t* skip = nullptr, int fin = FIN_NONE, int fin_arg = 0,
                          int nstore = NQ) {
-  Geom geo = make_geom(n, c->ng, c->gs);
+  Geom geo = make_geom(n, c->ng, c->gs, min_units(c));
   if (!geo.leaf && (size_t)geo.G * (size_t)nstore > c->spill_cap)
+    return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
+  if (geo.leaf && geo.logf > 0 && (size_t)geo.units * 32 * NQ > c->spill_cap)
     return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
   if constexpr (NQ <= 4) {
   if (!geo.leaf && geo.gs >= 32 && geo.K >= 2 && geo.K <= 8) {
@@ -977,7 +981,7 @@ extern "C" int pk_gs_stage1(pk_ctx* c, int64_t n, int32_t nb, const double* cons
   PK_CHECK_CTX(c);
   if (nb < 0 || (nb > 0 && (!basis || !partials))) return fail(PK_ERR_INVALID, "bad argument");
   if (nb == 0) return PK_OK;
-  PK_TRY(ensure_scratch(c, n, std::min(nb, multidot_nb_cap(c, n))));
+  PK_TRY(ensure_scratch(c, n, multidot_nb_cap(c, n)));  // padded NB <= cap
   return multidot_any(c, c->stream, n, nb, basis, v, partials, nb, 0);
 }
 

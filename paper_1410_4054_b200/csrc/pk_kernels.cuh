@@ -470,7 +470,7 @@ struct OpBicgA {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = 2;
-  static constexpr int kRowsPerThread = 2;
+  static constexpr int kRowsPerThread = 4;
   static constexpr int kSlots = S_;
   static constexpr int kWarpRows = 2;
   Csr<RowT> A;

@@ -60,12 +60,16 @@ struct Geom {
   int32_t leaf;    // 1 = LEAF mapping
   int32_t m;       // LEAF: leaves per lane thread (gs / 32)
   int32_t logm;
+  int32_t logf;    // LEAF: a group is split over F = 2^logf CTAs (units = n_groups F)
   int32_t tT;      // CHAIN group tree: threads = min(gs, kThreads)
   int32_t tm;      // CHAIN group tree: leaves per tree thread
   int32_t tlogm;
 };
 
-inline Geom make_geom(int64_t n, int32_t n_groups, int32_t gs) {
+// min_units: LEAF groups are split over F = 2^logf CTAs (each a contiguous
+// range of bit-reversed visits = a complete sub-tree) until n_groups F >=
+// min_units, so that few large groups still fill the GPU.
+inline Geom make_geom(int64_t n, int32_t n_groups, int32_t gs, int64_t min_units = 0) {
   Geom g{};
   g.n = n;
   g.n_groups = n_groups;
@@ -77,7 +81,9 @@ inline Geom make_geom(int64_t n, int32_t n_groups, int32_t gs) {
   if (g.leaf) {
     g.m = gs / 32;
     g.logm = ilog2_u((uint32_t)g.m);
-    g.units = n_groups;
+    g.logf = 0;
+    while ((int64_t)n_groups << g.logf < min_units && (1 << (g.logf + 1)) <= g.m) ++g.logf;
+    g.units = (int64_t)n_groups << g.logf;
   } else {
     g.units = (g.G + 31) / 32;
     g.tT = gs < kThreads ? gs : kThreads;
@@ -407,53 +413,90 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         ncomplete = g1 - g0;
       }
     } else {
-      // ---- LEAF: group g; the folding lane owns lanes {lane + 32 j} ----
-      const int g = (int)unit;
+      // ---- LEAF: group g, part cp of F; the folding lane owns lanes {lane + 32 j} ----
+      const int g = (int)(unit >> geo.logf);
+      const int F = 1 << geo.logf;
+      const int cp = (int)(unit & (F - 1));
+      const int msub = geo.m >> geo.logf;  // visits of this part: [cp msub, (cp + 1) msub)
       double out[QPW];
 #pragma unroll
       for (int i = 0; i < QPW; ++i) out[i] = 0.0;
-      for (int i0 = 0; i0 < geo.m; i0 += B) {
+      for (int i0 = 0; i0 < msub; i0 += B) {
         double* C = Cbuf + (bpar & 1u) * (B * NQ * 32);
         ++bpar;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int ii = warp + kWarps * u;
-          const int i = i0 + ii;
+          const int i = cp * msub + i0 + ii;
           const int64_t row = (int64_t)g * geo.gs + (int64_t)brev_bits((uint32_t)i, geo.logm) * 32 + lane;
           double c[NQ];
 #pragma unroll
           for (int q = 0; q < NQ; ++q) c[q] = 0.0;
-          if (i < geo.m && row < geo.n) row_contrib<NQ>(op, (uint32_t)row, c);
+          if (i0 + ii < msub && row < geo.n) row_contrib<NQ>(op, (uint32_t)row, c);
 #pragma unroll
           for (int q = 0; q < NQ; ++q) C[(ii * NQ + q) * 32 + lane] = c[q];
         }
         __syncthreads();
-        const int iend = (geo.m - i0) < B ? (geo.m - i0) : B;
+        const int iend = (msub - i0) < B ? (msub - i0) : B;
 #pragma unroll
         for (int w = 0; w < QPW; ++w) {
           const int q = warp + kWarps * w;
           if (q < NQ) {
             for (int ii = 0; ii < iend; ++ii) {
               const double x = C[(ii * NQ + q) * 32 + lane];
-              out[w] = geo.m > 1 ? leaf_push<NQ>(tail, q, lane, (uint32_t)(i0 + ii), x) : x;
+              out[w] = msub > 1 ? leaf_push<NQ>(tail, q, lane, (uint32_t)(i0 + ii), x) : x;
             }
           }
         }
       }
+      bool fin_group = true;
+      if (F > 1) {
+        // publish this part's sub-tree roots; the last part of the group
+        // merges the F roots in visit order (binary counter = halving tree)
 #pragma unroll
-      for (int w = 0; w < QPW; ++w) {
-        const int q = warp + kWarps * w;
-        if (q < NQ) {
-          double o = out[w];
+        for (int w = 0; w < QPW; ++w) {
+          const int q = warp + kWarps * w;
+          if (q < NQ) scr.spill[((unit * NQ) + q) * 32 + lane] = out[w];
+        }
+        __syncthreads();
+        if (tid == 0) {
+          unsigned tk = atomic_add_release(scr.gtick + g, 1u);
+          int lastp = (tk == (unsigned)F - 1);
+          if (lastp) scr.gtick[g] = 0u;
+          s_flag = lastp;
+        }
+        __syncthreads();
+        fin_group = s_flag != 0;
+        if (fin_group) {
 #pragma unroll
-          for (int sft = 16; sft >= 1; sft >>= 1) {
-            double t = __shfl_down_sync(kFull, o, sft);
-            if (lane < sft) o = add_rn(o, t);
+          for (int w = 0; w < QPW; ++w) {
+            const int q = warp + kWarps * w;
+            if (q < NQ) {
+              for (int c2 = 0; c2 < F; ++c2) {
+                const int64_t u2 = ((int64_t)g << geo.logf) + c2;
+                const double x = __ldcg(scr.spill + ((u2 * NQ) + q) * 32 + lane);
+                out[w] = leaf_push<NQ>(tail, q, lane, (uint32_t)c2, x);
+              }
+            }
           }
-          if (lane == 0 && part && q < nstore) part[(int64_t)g * ld + col0 + q] = o;
         }
       }
-      ncomplete = 1;
+      if (fin_group) {
+#pragma unroll
+        for (int w = 0; w < QPW; ++w) {
+          const int q = warp + kWarps * w;
+          if (q < NQ) {
+            double o = out[w];
+#pragma unroll
+            for (int sft = 16; sft >= 1; sft >>= 1) {
+              double t = __shfl_down_sync(kFull, o, sft);
+              if (lane < sft) o = add_rn(o, t);
+            }
+            if (lane == 0 && part && q < nstore) part[(int64_t)g * ld + col0 + q] = o;
+          }
+        }
+      }
+      ncomplete = fin_group ? 1 : 0;
     }
     // ---- global ticket: the CTA completing the last group finalizes ----
     if (ncomplete > 0) {

@@ -32,7 +32,7 @@ for w in $WHAT; do
         -o "$OUT/bicgstab_full" python tools/profile_target.py bicgstab 16 host > "$OUT/ncu.log" 2>&1
       echo "ncu rc=$?"; tail -3 "$OUT/ncu.log" ;;
     ncu_cg)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_reduce -s 40 -c 2 \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_reduce -s 25 -c 2 \
         -o "$OUT/cg_full" python tools/profile_target.py cg 16 host > "$OUT/ncu_cg.log" 2>&1
       echo "ncu_cg rc=$?"; tail -3 "$OUT/ncu_cg.log" ;;
     ncu_gmres)
