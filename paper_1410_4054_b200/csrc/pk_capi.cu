@@ -102,8 +102,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
   Op op = op0;
   op.scalars(sp);
   bool last = engine_run<NQ, U>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
-  if (last && fin != FIN_NONE && st && threadIdx.x < 32) finalize(st, fin, fin_arg, ing);  // warp 0 of the last CTA
+  if (last && fin != FIN_NONE && st && threadIdx.x < 32) {
+    // warp 0 of the last CTA; the engine's staging memory is free now
+    const Geom g2 = geo;
+    finalize(st, fin, fin_arg, ing, smem, (int)(engine_smem_bytes(g2, NQ, U) / sizeof(double)));
+  }
 }
+
+constexpr int kWarpStage2Doubles = 1024;  // stage-2 staging of the warp engine's finalizer
 
 // One warp per CTA, one unit per warp (CHAIN mapping with group_size >= 32).
 template <int NQ, int R, class Op>
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(32, 8)
   Op op = op0;
   op.scalars(sp);
   bool last = engine_warp_chain<NQ, R>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
-  if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing);
+  if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing, smem, kWarpStage2Doubles);
 }
 
 template <class Op>
@@ -129,7 +135,10 @@ __global__ void __launch_bounds__(256, 4) k_sweep(int64_t n, Op op, ScalarPtrs s
   sweep_rows(n, op);
 }
 
-__global__ void k_finalize(SolveState* st, int fin, int arg) { finalize(st, fin, arg, false); }
+__global__ void k_finalize(SolveState* st, int fin, int arg) {
+  __shared__ double buf[1024];
+  finalize(st, fin, arg, false, buf, 1024);
+}
 
 // totals[q] = serial sum of column q (reduce_stage2 / in-kernel finalize)
 __global__ void k_stage2(const double* part, int ng, int ld, int nq, double* out) {
@@ -306,6 +315,21 @@ static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
 
 static Scratch scratch_of(const pk_ctx* c) { return Scratch{c->spill, c->gtick, c->ticket}; }
 
+// Raise a kernel's dynamic shared-memory limit when a launch needs more than
+// the default 48 KB minus its static shared memory (the finalizer's 8 KB
+// stage-2 staging buffer lives there); once per instantiation and size.
+template <class K>
+static int allow_dynamic_smem(K kern, size_t dyn) {
+  static size_t granted = 0;  // per template instantiation
+  if (dyn <= granted) return PK_OK;
+  cudaFuncAttributes fa;
+  PK_CUDA(cudaFuncGetAttributes(&fa, kern));
+  if (dyn + fa.sharedSizeBytes > 48 * 1024)
+    PK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+  granted = dyn;
+  return PK_OK;
+}
+
 template <class K>
 static int engine_grid(const pk_ctx* c, K kern, size_t smem, int64_t units, int threads = kThreads) {
   int occ = 0;
@@ -347,9 +371,9 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
     // for short chains (small, latency-bound systems, e.g. CG 512^2: 20.6 vs
     // 26.8 us/iter); long chains keep the CTA engine (C2: 44.7 vs 63.8 us)
     constexpr int R = WarpRows<Op>::value;
-    const size_t wsm = warp_chain_smem_bytes(geo, NQ);
+    const size_t wsm = std::max(warp_chain_smem_bytes(geo, NQ), (size_t)kWarpStage2Doubles * sizeof(double));
     auto kw = k_reduce_warp<NQ, R, Op>;
-    if (wsm + 1024 > 48 * 1024) PK_CUDA(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    PK_TRY(allow_dynamic_smem(kw, wsm));
     kw<<<(unsigned)geo.units, 32, wsm, s>>>(geo, op, sp, part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin,
                                             fin_arg);
     cudaError_t e = cudaGetLastError();
@@ -360,10 +384,8 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
   size_t smem = engine_smem_bytes(geo, NQ, U);
   constexpr int MINB = NQ > 8 ? 1 : (NQ > 4 ? 2 : Op::kMinBlocks);
   auto kern = k_reduce<NQ, U, MINB, Op>;
-  if (smem + 1024 > 48 * 1024) {
-    if (smem > 200 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
-    PK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  }
+  if (smem > 200 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
+  PK_TRY(allow_dynamic_smem(kern, smem));
   const int grid = engine_grid(c, kern, smem, geo.units);
   kern<<<grid, kThreads, smem, s>>>(geo, op, sp, part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin,
                                     fin_arg);
@@ -484,8 +506,13 @@ static int multidot_t(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double
 // Largest NB whose shared-memory footprint fits for this geometry.
 static int multidot_nb_cap(const pk_ctx* c, int64_t n) {
   Geom geo = make_geom(n, c->ng, c->gs);
+  // at most 16 quantities per pass: wider passes need so much staging smem
+  // (and registers) that only 1-2 CTAs fit per SM; re-reading v per pass is
+  // cheaper than that loss of occupancy (GMRES(30) 128^3: measured)
+  const char* ev = getenv("PK_MULTIDOT_CAP");
+  const int top = ev ? atoi(ev) : 16;
   for (int nb : {32, 16, 8, 4, 2, 1}) {
-    if (engine_smem_bytes(geo, nb, 1) <= 192 * 1024) return nb;
+    if (nb <= top && engine_smem_bytes(geo, nb, 1) <= 192 * 1024) return nb;
   }
   return 1;
 }

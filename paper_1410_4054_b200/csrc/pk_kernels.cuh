@@ -110,23 +110,63 @@ __device__ inline void cg_scalars(SolveState* st, double rr, double pap, double 
   set_cond(st, stop ? 0u : 1u, ing);
 }
 
-__device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
+// Serial stage 2 (linalg.py:311-320) of NC partial columns, executed by one
+// warp: chunks of the partials are staged through shared memory with
+// coalesced warp-wide L2 loads, then lane c adds column c in group order
+// (the reference's left-to-right chain); every lane receives the totals.
+struct S2Col {
+  const double* part;
+  int ld;
+  int col;
+};
+
+template <int NC>
+__device__ __noinline__ void stage2_warp(const S2Col* cols, int ng, double* out, double* buf, int buf_d) {
+  const int CH = buf_d / NC;  // groups per chunk of the (dynamic) staging buffer
+  const int lane = threadIdx.x & 31;
+  double tot = 0.0;
+  for (int g0 = 0; g0 < ng; g0 += CH) {
+    const int cnt = (ng - g0) < CH ? (ng - g0) : CH;
+    __syncwarp();
+    for (int idx = lane; idx < cnt * NC; idx += 32) {
+      const int c = idx / cnt, g = idx - c * cnt;
+      buf[c * CH + g] = __ldcg(cols[c].part + (int64_t)(g0 + g) * cols[c].ld + cols[c].col);
+    }
+    __syncwarp();
+    if (lane < NC) {
+      const double* b = buf + lane * CH;
+      int g = 0;
+      for (; g + 8 <= cnt; g += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = b[g + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) tot = add_rn(tot, v[u]);
+      }
+      for (; g < cnt; ++g) tot = add_rn(tot, b[g]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) out[c] = __shfl_sync(0xffffffffu, tot, c);
+  __syncwarp();
+}
+
+// buf / buf_d: shared-memory staging for the stage-2 loads (>= 32 doubles;
+// the launching kernel's dynamic shared memory, free by the time it finalizes)
+__device__ inline void finalize(SolveState* st, int fin, int arg, bool ing, double* buf, int buf_d) {
   const int th = threadIdx.x & 31;  // executed by one warp
   const int ng = st->n_groups;
-  __shared__ double tot[32];
+  double tot[4];
   switch (fin) {
     case FIN_CG_SETUP: {
-      if (th == 0) tot[0] = stage2_col(st->p_rr, ng, 1, 0);
-      if (th == 1) tot[1] = stage2_col(st->p_two, ng, 2, 0);
-      if (th == 2) tot[2] = stage2_col(st->p_two, ng, 2, 1);
-      if (th == 3) tot[3] = stage2_col(st->p_bb, ng, 1, 0);
-      __syncwarp();
+      const S2Col cs[4] = {{st->p_rr, 1, 0}, {st->p_two, 2, 0}, {st->p_two, 2, 1}, {st->p_bb, 1, 0}};
+      stage2_warp<4>(cs, ng, tot, buf, buf_d);
       if (th == 0) cg_scalars(st, tot[0], tot[1], tot[2], true, tot[3], ing);
       break;
     }
     case FIN_CG_FUSED: {
-      if (th < 3) tot[th] = stage2_col(st->p_three, ng, 3, th);
-      __syncwarp();
+      const S2Col cs[3] = {{st->p_three, 3, 0}, {st->p_three, 3, 1}, {st->p_three, 3, 2}};
+      stage2_warp<3>(cs, ng, tot, buf, buf_d);
       if (th == 0) {
         st->parity ^= 1;
         cg_scalars(st, tot[0], tot[1], tot[2], false, 0.0, ing);
@@ -134,9 +174,8 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
       break;
     }
     case FIN_BICG_SETUP: {
-      if (th == 0) tot[0] = stage2_col(st->p_pair, ng, 2, 0);
-      if (th == 1) tot[1] = stage2_col(st->p_bb, ng, 1, 0);
-      __syncwarp();
+      const S2Col cs[2] = {{st->p_pair, 2, 0}, {st->p_bb, 1, 0}};
+      stage2_warp<2>(cs, ng, tot, buf, buf_d);
       if (th != 0) return;
       double rr = tot[0];
       double nb = msqrt(tot[1]);
@@ -152,8 +191,8 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     }
     case FIN_BICG_ALPHA: {
       // fused_bicgstab_s_update's in-kernel alpha (fused.py:172-176)
-      if (th < 2) tot[th] = stage2_col(st->p_pair, ng, 2, th);
-      __syncwarp();
+      const S2Col cs[2] = {{st->p_pair, 2, 0}, {st->p_pair, 2, 1}};
+      stage2_warp<2>(cs, ng, tot, buf, buf_d);
       if (th != 0) return;
       if (arg) st->parity ^= 1;
       double rho = tot[0], d = tot[1];
@@ -170,8 +209,8 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     }
     case FIN_BICG_TAIL: {
       // solvers.py:647-684
-      if (th < 4) tot[th] = stage2_col(st->p_quad, ng, 4, th);
-      __syncwarp();
+      const S2Col cs[4] = {{st->p_quad, 4, 0}, {st->p_quad, 4, 1}, {st->p_quad, 4, 2}, {st->p_quad, 4, 3}};
+      stage2_warp<4>(cs, ng, tot, buf, buf_d);
       if (th != 0) return;
       double ss = tot[0], ass = tot[1], asas = tot[2], asr = tot[3], apr = st->apr;
       st->ss = ss; st->ass = ass; st->asas = asas; st->asr = asr;
@@ -221,9 +260,8 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
       break;
     }
     case FIN_GM_RHO: {
-      if (th == 0) tot[0] = stage2_col(st->p_rr, ng, 1, 0);
-      if (th == 1 && arg) tot[1] = stage2_col(st->p_bb, ng, 1, 0);
-      __syncwarp();
+      const S2Col cs[2] = {{st->p_rr, 1, 0}, {st->p_bb, 1, 0}};
+      stage2_warp<2>(cs, ng, tot, buf, buf_d);
       if (th != 0) return;
       if (arg) {
         double nb = msqrt(tot[1]);
@@ -234,8 +272,10 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     }
     case FIN_GM_NORM: {
       // arg = step index i (1-based)
+      const S2Col cs[1] = {{st->p_ww, 1, 0}};
+      stage2_warp<1>(cs, ng, tot, buf, buf_d);
       if (th == 0) {
-        double nrm = msqrt(stage2_col(st->p_ww, ng, 1, 0));
+        double nrm = msqrt(tot[0]);
         st->nrm = nrm;
         if (nrm < st->btol_loop || nrm == 0.0) {
           st->lucky = 1;
@@ -248,22 +288,31 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing) {
     }
     case FIN_GM_COEF: {
       // arg = step index i (>= 2): columns 0..i-2 of p_coef
-      for (int j = th; j < arg - 1; j += 32) {
-        double c = stage2_col(st->p_coef, ng, st->m, j);
-        st->coef[j] = c;
-        st->R[(int64_t)j * st->m + (arg - 1)] = c;
+      for (int j0 = 0; j0 < arg - 1; j0 += 4) {
+        const int nj = (arg - 1 - j0) < 4 ? (arg - 1 - j0) : 4;
+        const S2Col cs[4] = {{st->p_coef, st->m, j0}, {st->p_coef, st->m, j0 + (nj > 1)},
+                             {st->p_coef, st->m, j0 + 2 * (nj > 2)}, {st->p_coef, st->m, j0 + 3 * (nj > 3)}};
+        stage2_warp<4>(cs, ng, tot, buf, buf_d);
+        if (th < nj) {
+          st->coef[j0 + th] = tot[th];
+          st->R[(int64_t)(j0 + th) * st->m + (arg - 1)] = tot[th];
+        }
       }
       break;
     }
     case FIN_GM_XI: {
+      const S2Col cs[1] = {{st->p_xi + (int64_t)(arg - 1) * ng, 1, 0}};
+      stage2_warp<1>(cs, ng, tot, buf, buf_d);
       if (th == 0) {
-        st->xi[arg - 1] = stage2_col(st->p_xi + (int64_t)(arg - 1) * ng, ng, 1, 0);
+        st->xi[arg - 1] = tot[0];
         st->step = arg;
       }
       break;
     }
     case FIN_DOTV: {
-      if (th == 0) st->dotv = stage2_col(st->p_bb, ng, 1, 0);
+      const S2Col cs[1] = {{st->p_bb, 1, 0}};
+      stage2_warp<1>(cs, ng, tot, buf, buf_d);
+      if (th == 0) st->dotv = tot[0];
       break;
     }
     default:

@@ -100,7 +100,7 @@ __host__ __device__ inline size_t engine_tail_doubles(const Geom& g, int nq) {
   return g.leaf ? (g.m > 1 ? (size_t)(g.logm + 1) * nq * 32 : 0)
                 : (size_t)nq * g.tT + (g.tm > 1 ? (size_t)(g.tlogm + 1) * nq * g.tT : 0);
 }
-inline size_t engine_smem_bytes(const Geom& g, int nq, int U) {
+__host__ __device__ inline size_t engine_smem_bytes(const Geom& g, int nq, int U) {
   return ((size_t)2 * kWarps * U * nq * 32 + engine_tail_doubles(g, nq)) * sizeof(double);
 }
 

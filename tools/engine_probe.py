@@ -37,7 +37,11 @@ print(json.dumps({"method": method, "side": side, "graph_us_per_iter": rg.loop_s
 if __name__ == "__main__":
     runs = sys.argv[1:] or ["bicgstab:1024:0"]
     for spec in runs:
-        method, side, flags = spec.split(":")
-        out = subprocess.run([sys.executable, "-c", CHILD, method, side], capture_output=True, text=True)
+        method, side, tag = spec.split(":")
+        env = dict(os.environ)
+        if "=" in tag:  # e.g. PK_MULTIDOT_CAP=16
+            k, v = tag.split("=", 1)
+            env[k] = v
+        out = subprocess.run([sys.executable, "-c", CHILD, method, side], capture_output=True, text=True, env=env)
         line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr.strip()[-400:]
-        print(f"flags={flags} {line}", flush=True)
+        print(f"{tag} {line}", flush=True)
