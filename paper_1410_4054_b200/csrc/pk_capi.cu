@@ -70,6 +70,7 @@ struct pk_ctx {
   size_t spill_cap = 0;
   unsigned* gtick = nullptr;      // per-group tickets [ng] + global ticket
   unsigned* ticket = nullptr;
+  std::vector<pk_ctx*> workers;   // pk_solve_batch worker contexts (kept across calls)
 };
 
 struct pk_mat {
@@ -286,9 +287,17 @@ __global__ void k_row_max(const int64_t* counts, int64_t n, unsigned long long* 
   unsigned long long m = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     m = max(m, (unsigned long long)counts[i]);
-  // warp maximum first: one atomic per warp instead of one per thread
+  // block maximum first: same-address 64-bit atomics serialise in one L2
+  // slice (one per warp cost ~400 us at 1M rows), so one atomic per block
+  __shared__ unsigned long long wm[32];
   for (int s = 16; s >= 1; s >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, s));
-  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0ull;
+    for (int s = 16; s >= 1; s >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, s));
+    if (threadIdx.x == 0) atomicMax(mx, m);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -620,6 +629,8 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
 
 extern "C" int pk_ctx_destroy(pk_ctx* c) {
   if (!c) return PK_OK;
+  for (pk_ctx* w : c->workers) pk_ctx_destroy(w);
+  c->workers.clear();
   cudaSetDevice(c->device);
   if (c->own) cudaStreamSynchronize(c->own);
   if (c->scratch) cudaFree(c->scratch);
@@ -820,7 +831,7 @@ static int gen_stencil(pk_ctx* c, int32_t family, const int64_t* dims, int32_t n
   PK_CUDA(cudaMemsetAsync(dmax, 0, 8, s));
   int g = grid_elem(c, n, 256);
   k_gen_count<<<g, 256, 0, s>>>(n, sp, counts);
-  k_row_max<<<g, 256, 0, s>>>(counts, n, dmax);
+  k_row_max<<<std::min(g, c->sm_count * 2), 256, 0, s>>>(counts, n, dmax);
   k_scan_block<<<(unsigned)nblk, 1024, 0, s>>>(counts, incl, n, bsum);
   // scan block sums on the host (nblk <= 2M)
   std::vector<int64_t> hb((size_t)nblk);

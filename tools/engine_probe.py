@@ -12,7 +12,9 @@ sys.path.insert(0, ".")
 import paper_1410_4054_b200 as pk
 from paper_1410_4054_b200.solvers import solve_resident
 method, side = sys.argv[1], int(sys.argv[2])
-ctx = pk.ExecutionContext(128, 256, device=0)
+import os
+geom = tuple(int(v) for v in os.environ.get("PK_GEOM", "128x256").split("x"))
+ctx = pk.ExecutionContext(*geom, device=0)
 if method == "bicgstab":
     dm, b = pk.convdiff2d(side, device=True, context=ctx)
 elif method == "cg3d":
