@@ -13,6 +13,8 @@ import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libpk_b200.so"
+if os.environ.get("PK_LIB_VARIANT"):  # engine experiments: libpk_b200_<variant>.so built by tools/build_variants.sh
+    LIB_PATH = LIB_PATH.with_name(f"libpk_b200_{os.environ['PK_LIB_VARIANT']}.so")
 
 PK_OK, PK_ERR_INVALID, PK_ERR_CUDA, PK_ERR_NOMEM, PK_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 TERM_NAMES = {0: "converged", 1: "max_iter", 2: "breakdown", 3: "lucky_breakdown"}

@@ -28,6 +28,10 @@
 #include "pk_reduce.cuh"
 #include "pk_state.cuh"
 
+#ifndef PK_BICGB_MINB
+#define PK_BICGB_MINB 4
+#endif
+
 namespace pk {
 
 // ---------------------------------------------------------------------------
@@ -475,7 +479,7 @@ template <typename RowT_, int S_>
 struct OpBicgB {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
-  static constexpr int kMinBlocks = 4;
+  static constexpr int kMinBlocks = PK_BICGB_MINB;
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
   Csr<RowT> A;
