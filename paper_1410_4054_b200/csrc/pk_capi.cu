@@ -17,6 +17,7 @@
 #include <string>
 #include <thread>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "pipekrylov_b200.h"
@@ -52,6 +53,27 @@ static int fail(int code, const std::string& msg) {
     if (rc_ != PK_OK) return rc_; \
   } while (0)
 
+// Kernel launch, with the programmatic-dependent-launch attribute when pdl.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  if (!pdl) {
+    kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---------------------------------------------------------------------------
 // objects
 // ---------------------------------------------------------------------------
@@ -71,6 +93,7 @@ struct pk_ctx {
   unsigned* gtick = nullptr;      // per-group tickets [ng] + global ticket
   unsigned* ticket = nullptr;
   std::vector<pk_ctx*> workers;   // pk_solve_batch worker contexts (kept across calls)
+  bool pdl = false;               // PK_PDL=1: programmatic stream serialization (measured slower, off)
 };
 
 struct pk_mat {
@@ -91,11 +114,21 @@ static int set_device(int dev) {
 // kernels
 // ---------------------------------------------------------------------------
 
+// Programmatic dependent launch: every loop kernel lets its successor's CTAs
+// launch as soon as all of its own CTAs are resident (they then occupy the
+// slots the partially filled last wave and the finalizer tail leave idle),
+// and waits for its predecessor's completion + memory flush before touching
+// anything.  Both are no-ops for launches without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <int NQ, int U, int MINB, class Op>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_reduce(const __grid_constant__ Geom geo, const __grid_constant__ Op op0, ScalarPtrs sp, double* part, int ld,
              int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin, int fin_arg) {
   extern __shared__ double smem[];
+  pdl_wait();
+  pdl_trigger();
   if (skip && *(volatile const int32_t*)skip) return;
   const bool ing = (gate & GATE_IN_GRAPH) != 0;
   gate &= 0xff;
@@ -119,6 +152,8 @@ __global__ void __launch_bounds__(32, 8)
                   int ld, int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin,
                   int fin_arg) {
   extern __shared__ double smem[];
+  pdl_wait();
+  pdl_trigger();
   if (skip && *(volatile const int32_t*)skip) return;
   const bool ing = (gate & GATE_IN_GRAPH) != 0;
   gate &= 0xff;
@@ -131,6 +166,8 @@ __global__ void __launch_bounds__(32, 8)
 
 template <class Op>
 __global__ void __launch_bounds__(256, 4) k_sweep(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
+  pdl_wait();
+  pdl_trigger();
   if (st && !gate_open(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0)) return;
   op.scalars(sp);
   sweep_rows(n, op);
@@ -383,9 +420,8 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
     const size_t wsm = std::max(warp_chain_smem_bytes(geo, NQ), (size_t)kWarpStage2Doubles * sizeof(double));
     auto kw = k_reduce_warp<NQ, R, Op>;
     PK_TRY(allow_dynamic_smem(kw, wsm));
-    kw<<<(unsigned)geo.units, 32, wsm, s>>>(geo, op, sp, part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin,
-                                            fin_arg);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_k(c->pdl, kw, dim3((unsigned)geo.units), dim3(32), wsm, s, geo, op, sp, part, ld, col0,
+                             nstore, scratch_of(c), st, gate, skip, fin, fin_arg);
     if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("warp engine launch: ") + cudaGetErrorString(e));
     return PK_OK;
   }
@@ -396,9 +432,8 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
   if (smem > 200 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
   PK_TRY(allow_dynamic_smem(kern, smem));
   const int grid = engine_grid(c, kern, smem, geo.units);
-  kern<<<grid, kThreads, smem, s>>>(geo, op, sp, part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin,
-                                    fin_arg);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(c->pdl, kern, dim3(grid), dim3(kThreads), smem, s, geo, op, sp, part, ld, col0, nstore,
+                           scratch_of(c), st, gate, skip, fin, fin_arg);
   if (e != cudaSuccess)
     return fail(PK_ERR_CUDA, std::string("engine launch (nq=") + std::to_string(NQ) + ", smem=" +
                                  std::to_string(smem) + ", grid=" + std::to_string(grid) + ", leaf=" +
@@ -410,8 +445,8 @@ template <class Op>
 static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp = ScalarPtrs{},
                         SolveState* st = nullptr, int gate = GATE_NONE) {
   auto kern = k_sweep<Op>;
-  kern<<<engine_grid(c, kern, 0, (n + 255) / 256, 256), 256, 0, s>>>(n, op, sp, st, gate);
-  PK_CUDA(cudaGetLastError());
+  PK_CUDA(launch_k(c->pdl, kern, dim3(engine_grid(c, kern, 0, (n + 255) / 256, 256)), dim3(256), 0, s, n, op, sp, st,
+                   gate));
   return PK_OK;
 }
 
@@ -617,6 +652,7 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
     return fail(PK_ERR_CUDA, std::string("context allocation: ") + cudaGetErrorString(e));
   }
   c->stream = c->own;
+  if (const char* e2 = getenv("PK_PDL")) c->pdl = atoi(e2) != 0;
   // keep freed workspace memory in the stream-ordered pool between solves
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

@@ -87,6 +87,20 @@ def test_loop_modes_identical(pk, mode):
         assert_identical(res, oracle_run(method, a, b, (128, 256)))
 
 
+@pytest.mark.parametrize("unroll", ["1", "3", "8"])
+def test_graph_unroll_identical(pk, unroll, monkeypatch):
+    """Iterations per WHILE-body execution (PK_UNROLL, read when the loop
+    graph is built): stops inside an unrolled body must leave no trace --
+    converged, max_iter and fixed-iteration runs with iteration counts that
+    are not multiples of the unroll."""
+    monkeypatch.setenv("PK_UNROLL", unroll)
+    a, b = pk.poisson2d_grid(50)
+    for method, kw, okw in (("cg", {}, {}), ("bicgstab", {}, {}), ("cg", {"max_iterations": 13}, {"max_iterations": 13}),
+                            ("bicgstab", {"fixed_iterations": 7, "max_iterations": 7}, {"fixed": 7, "max_iterations": 7})):
+        res = pk.SOLVERS[(method, "pipelined")](a, b, config=pk.SolverConfig(**kw))
+        assert_identical(res, oracle_run(method, a, b, (128, 256), **okw))
+
+
 def test_reruns_bit_identical(pk):
     a, b = pk.convdiff2d(80)
     for key, solver in pk.SOLVERS.items():

@@ -41,9 +41,10 @@ if __name__ == "__main__":
     for spec in runs:
         method, side, tag = spec.split(":")
         env = dict(os.environ)
-        if "=" in tag:  # e.g. PK_MULTIDOT_CAP=16
-            k, v = tag.split("=", 1)
-            env[k] = v
+        for kv in tag.split(","):  # e.g. PK_MULTIDOT_CAP=16,PK_PDL=0
+            if "=" in kv:
+                k, v = kv.split("=", 1)
+                env[k] = v
         out = subprocess.run([sys.executable, "-c", CHILD, method, side], capture_output=True, text=True, env=env)
         line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr.strip()[-400:]
         print(f"{tag} {line}", flush=True)
