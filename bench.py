@@ -4,7 +4,7 @@ Workload (BASELINE.json configs[1], the single-B200 headline): pipelined
 BiCGStab on the 2D first-order upwind convection-diffusion operator, 1024 x
 1024 grid (n = 1 048 576, nnz = 5 238 784), fp64, reference default reduction
 geometry 128 x 256 (bit-identical to the reference CPU implementation at that
-geometry).  A "step" is one pipelined BiCGStab iteration (2 fused kernels);
+geometry).  A "step" is one pipelined BiCGStab iteration (3 kernels);
 the K timed steps are one fixed-iteration device loop (conditional-WHILE CUDA
 graph) timed with CUDA events on its stream, setup excluded -- the paper's /
 reference's loop_seconds protocol (solvers.py:632-695).
@@ -156,12 +156,13 @@ def ncu_traffic(kernel):
 
 
 def kernel_roofline(pk, dm, ctx, torch, b, iters=200):
-    """Per-kernel CUDA-event times of the two loop kernels (host-enqueued
+    """Per-kernel CUDA-event times of the three loop kernels (host-enqueued
     loop with PK_FLAG_PROFILE, events on the launching stream), against the
     measured HBM copy peak.  Algorithmic bytes per launch (int32 indices,
     fp64 values, every vector read/written once):
-      As-SpMV  (OpBicgB): B_CSR + 32 n   (read r, Ap, r0*; write As)
-      xrp+Ap   (OpBicgA): B_CSR + 80 n   (read x, r, p, Ap, As, r0*; write x, r, p, Ap)"""
+      As-SpMV  (OpBicgB):        B_CSR + 32 n   (read r, Ap, r0*; write As)
+      Ap'-SpMV (OpBicgApNext):   B_CSR + 32 n   (read p', r', r0*; write Ap')
+      xrp      (OpBicgXrpSweep): 64 n           (read x, r, p, Ap, As; write x, r', p')"""
     from paper_1410_4054_b200.solvers import solve_resident
 
     n = dm.n_rows
@@ -171,7 +172,8 @@ def kernel_roofline(pk, dm, ctx, torch, b, iters=200):
     ks, kl = res.diagnostics["kernel_seconds"], res.diagnostics["kernel_launches"]
     bc = b_csr(n, dm.nnz)
     kernels = [("k_reduce<OpBicgB> (s-update + As = A s + 4 dots)", bc + 32 * n, ks[0], kl[0]),
-               ("k_reduce<OpBicgA> (xrp update + Ap = A p + 2 dots)", bc + 80 * n, ks[1], kl[1])]
+               ("k_reduce<OpBicgApNext> (Ap' = A p' + 2 dots)", bc + 32 * n, ks[1], kl[1]),
+               ("k_sweep<OpBicgXrpSweep> (xrp update)", 64 * n, ks[2], kl[2])]
     peak, kind = peaks()
     rows = []
     for name, alg, sec, cnt in kernels:
@@ -358,8 +360,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         loop_s = float(t.item())
     us_iter = loop_s / args.steps * 1e6
-    # algorithmic bytes of the fused 2-kernel iteration (see kernel_roofline)
-    iter_bytes = 2 * b_csr(n, nnz) + 112 * n
+    # algorithmic bytes of the 3-kernel iteration (see kernel_roofline); the
+    # fused 2-kernel form would move 16 n fewer (reported beside it)
+    iter_bytes = 2 * b_csr(n, nnz) + 128 * n
     peak, peak_kind = peaks()
 
     if rank != 0:
@@ -398,13 +401,15 @@ def main():
         "config": config_block(),
         "iteration_roofline": {"bytes_per_iteration": iter_bytes,
                                "reference_4kernel_bytes": 2 * b_csr(n, nnz) + 144 * n,
+                               "fused_2kernel_bytes": 2 * b_csr(n, nnz) + 112 * n,
+                               "achieved_gbs_vs_fused_bytes": round((2 * b_csr(n, nnz) + 112 * n) / (us_iter * 1e-6) / 1e9, 1),
                                "achieved_gbs": round(iter_bytes / (us_iter * 1e-6) / 1e9, 1),
                                "frac": round(iter_bytes / (us_iter * 1e-6) / 1e9 / peak, 4)},
         "roofline": roof,
         "e2e": {"value": round(e2e_us, 3), "unit": "us/iter", "iterations_per_call": e2e_iters,
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 8 * e2e_iters},
-        # loop kernels (2 per iteration) + the first As-SpMV and the final update
-        "gpu_launches": int(res.diagnostics.get("launches_per_iteration", 2)) * args.steps,
+        # loop kernels (3 per iteration)
+        "gpu_launches": int(res.diagnostics.get("launches_per_iteration", 3)) * args.steps,
         "clocks": clk.summary(),
         "termination": res.termination,
     }

@@ -472,6 +472,74 @@ struct OpCgFused {
   }
 };
 
+// Split form of OpCgFused (PK_CG_SPLIT=1): the CG vector update as an
+// elementwise sweep (cur -> next halves) and a one-gather SpMV of p' with the
+// same contributions [r'.r', Ap'.p', Ap'.Ap'].
+struct OpCgXSweep {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
+  double* x;
+  double* r[2];
+  double* p[2];
+  double* ap[2];
+  double alpha, beta;
+  const double* rc;
+  const double* pc;
+  const double* apc;
+  double* rn_;
+  double* pn_;
+  struct Item { double x, r, p, ap; };
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
+    it.x = __ldg(x + i); it.r = __ldg(rc + i); it.p = __ldg(pc + i); it.ap = __ldg(apc + i);
+  }
+  template <int M>
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&)[M]) const {
+    double xn = add_rn(it.x, mul_rn(alpha, it.p));
+    double rn = sub_rn(it.r, mul_rn(alpha, it.ap));
+    double pn = add_rn(mul_rn(it.p, beta), rn);
+    x[i] = xn; rn_[i] = rn; pn_[i] = pn;
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    alpha = ld_scalar(sp.a, alpha);
+    beta = ld_scalar(sp.b, beta);
+    const int cur = ld_par(sp.par);
+    rc = cur ? r[1] : r[0]; pc = cur ? p[1] : p[0]; apc = cur ? ap[1] : ap[0];
+    rn_ = cur ? r[0] : r[1]; pn_ = cur ? p[0] : p[1];
+  }
+};
+
+template <typename RowT_, int S_>
+struct OpCgApNext {
+  using RowT = RowT_;
+  static constexpr bool kSpmv = true;
+  static constexpr int kMinBlocks = 4;
+  static constexpr int kRowsPerThread = 2;
+  static constexpr int kSlots = S_;
+  Csr<RowT> A;
+  double* r[2];
+  double* p[2];
+  double* ap[2];
+  const double* rn;
+  const double* pn;
+  double* apn;
+  struct Item { double r, p; };
+  struct Gat { double p; };
+  __device__ __forceinline__ void load(uint32_t row, Item& it) const { it.r = __ldg(rn + row); it.p = __ldg(pn + row); }
+  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const { g.p = __ldg(pn + col); }
+  __device__ __forceinline__ double gval(const Gat& g) const { return g.p; }
+  template <int M>
+  __device__ __forceinline__ void compute(uint32_t row, Item& it, double q, double (&c)[M]) const {
+    apn[row] = q;
+    c[0] = mul_rn(it.r, it.r);
+    c[1] = mul_rn(q, it.p);
+    c[2] = mul_rn(q, q);
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    const int cur = ld_par(sp.par);
+    rn = cur ? r[0] : r[1]; pn = cur ? p[0] : p[1]; apn = cur ? ap[0] : ap[1];
+  }
+};
+
 // BiCGStab second SpMV with the s-update folded in (fused.py:154-182 + 86-120):
 //   s = r - a Ap (recomputed at every gathered column, never stored);
 //   As = A s;  contributions [s.s, As.s, As.As, As.r0*].
@@ -571,6 +639,81 @@ struct OpBicgA {
     const int cur = ld_par(sp.par);
     rc = cur ? r[1] : r[0]; pc = cur ? p[1] : p[0]; apc = cur ? ap[1] : ap[0];
     rn_ = cur ? r[0] : r[1]; pn_ = cur ? p[0] : p[1]; apn_ = cur ? ap[0] : ap[1];
+  }
+};
+
+// Split form of OpBicgA (the default BiCGStab body): the xrp update as a
+// lean elementwise sweep (OpBicgXrpSweep, cur -> next half of the ping-pong
+// pairs) followed by a one-gather SpMV of p' carrying the same two
+// contributions [r'.r0*, Ap'.r0*] (OpBicgApNext).  Same IEEE operations on
+// the same inputs as OpBicgA, so the same bits.  Measured (C2): the fused
+// OpBicgA's four gathers per nonzero keep it at 2 CTAs/SM and 2.3 TB/s
+// (64 us); sweep + light SpMV take 15 + 34 us.
+struct OpBicgXrpSweep {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 4;
+  double* x;
+  double* r[2];
+  double* p[2];
+  double* ap[2];
+  const double* __restrict__ as;
+  double alpha, omega, beta;
+  const double* rc;
+  const double* pc;
+  const double* apc;
+  double* rn_;
+  double* pn_;
+  struct Item { double x, r, p, ap, as; };
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
+    it.x = __ldg(x + i); it.r = __ldg(rc + i); it.p = __ldg(pc + i); it.ap = __ldg(apc + i); it.as = __ldg(as + i);
+  }
+  template <int M>
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&)[M]) const {
+    double s = sub_rn(it.r, mul_rn(alpha, it.ap));
+    double xn = add_rn(it.x, add_rn(mul_rn(alpha, it.p), mul_rn(omega, s)));
+    double rn = sub_rn(s, mul_rn(omega, it.as));
+    double pn = add_rn(mul_rn(sub_rn(it.p, mul_rn(omega, it.ap)), beta), rn);
+    x[i] = xn; rn_[i] = rn; pn_[i] = pn;
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    alpha = ld_scalar(sp.a, alpha);
+    omega = ld_scalar(sp.b, omega);
+    beta = ld_scalar(sp.c, beta);
+    const int cur = ld_par(sp.par);
+    rc = cur ? r[1] : r[0]; pc = cur ? p[1] : p[0]; apc = cur ? ap[1] : ap[0];
+    rn_ = cur ? r[0] : r[1]; pn_ = cur ? p[0] : p[1];
+  }
+};
+
+template <typename RowT_, int S_>
+struct OpBicgApNext {
+  using RowT = RowT_;
+  static constexpr bool kSpmv = true;
+  static constexpr int kMinBlocks = 4;
+  static constexpr int kRowsPerThread = 2;
+  static constexpr int kSlots = S_;
+  Csr<RowT> A;
+  double* r[2];
+  double* p[2];
+  double* ap[2];
+  const double* __restrict__ r0;
+  const double* rn;
+  const double* pn;
+  double* apn;
+  struct Item { double r, r0; };
+  struct Gat { double p; };
+  __device__ __forceinline__ void load(uint32_t row, Item& it) const { it.r = __ldg(rn + row); it.r0 = __ldg(r0 + row); }
+  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const { g.p = __ldg(pn + col); }
+  __device__ __forceinline__ double gval(const Gat& g) const { return g.p; }
+  template <int M>
+  __device__ __forceinline__ void compute(uint32_t row, Item& it, double q, double (&c)[M]) const {
+    apn[row] = q;
+    c[0] = mul_rn(it.r, it.r0);
+    c[1] = mul_rn(q, it.r0);
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    const int cur = ld_par(sp.par);
+    rn = cur ? r[0] : r[1]; pn = cur ? p[0] : p[1]; apn = cur ? ap[0] : ap[1];
   }
 };
 

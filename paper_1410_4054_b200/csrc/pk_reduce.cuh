@@ -38,6 +38,10 @@
 
 #include <type_traits>
 
+#ifndef PK_SWEEP_V
+#define PK_SWEEP_V 4
+#endif
+
 namespace pk {
 
 constexpr int kWarps = 8;  // warps of an engine CTA
@@ -700,7 +704,23 @@ __device__ __forceinline__ bool engine_warp_chain(const Geom& geo, const Op& op,
 // Grid-stride thread-per-row sweep (no reduction): plain SpMV / updates.
 template <class Op>
 __device__ __forceinline__ void sweep_rows(int64_t n, const Op& op) {
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (!Op::kSpmv) {
+    // SWEEP_V rows per thread in flight (all loads issued before any compute)
+    constexpr int V = PK_SWEEP_V;
+    for (; row + (V - 1) * stride < n; row += V * stride) {
+      typename Op::Item it[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) op.load((uint32_t)(row + v * stride), it[v]);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        double c[1];
+        op.compute((uint32_t)(row + v * stride), it[v], c);
+      }
+    }
+  }
+  for (; row < n; row += stride) {
     double c[1];
     row_contrib<1>(op, (uint32_t)row, c);
   }

@@ -252,16 +252,20 @@ def _run(method: str, a, b, x0, config, context, debug):
 
 
 def cg_pipelined(a, b, x0=None, config=None, context=None, debug=False) -> SolverResult:
-    """Pipelined CG (solvers.py:395-469): ONE fused kernel per iteration (the
-    vector update folded into the SpMV by recompute-at-gather), the stage-2
-    reduction and alpha/beta/convergence finalized on the device."""
+    """Pipelined CG (solvers.py:395-469): below 2^20 rows ONE fused kernel per
+    iteration (the vector update folded into the SpMV by recompute-at-gather),
+    above it the update sweep + a one-gather SpMV (2 kernels, faster when
+    bandwidth-bound); the stage-2 reduction and alpha/beta/convergence are
+    finalized on the device either way."""
     return _run("cg", a, b, x0, config, context, debug)
 
 
 def bicgstab_pipelined(a, b, x0=None, config=None, context=None, debug=False) -> SolverResult:
-    """Pipelined BiCGStab (solvers.py:583-712): 2 fused kernels per iteration
-    (the reference's 4; s-update folded into the As-SpMV, xrp update into the
-    next iteration's Ap-SpMV)."""
+    """Pipelined BiCGStab (solvers.py:583-712): the s-update folded into the
+    As-SpMV; below 2^20 rows the xrp update is also folded into the next
+    iteration's Ap-SpMV (2 kernels per iteration), above it runs as a lean
+    elementwise sweep before a one-gather Ap-SpMV (3 kernels; faster on B200).
+    The reference emulates 4 launches + 1 transfer."""
     return _run("bicgstab", a, b, x0, config, context, debug)
 
 

@@ -101,6 +101,24 @@ def test_graph_unroll_identical(pk, unroll, monkeypatch):
         assert_identical(res, oracle_run(method, a, b, (128, 256), **okw))
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_split_and_fused_bodies_identical(pk, split, monkeypatch):
+    """Loop bodies: fused recompute-at-gather kernels (OpCgFused / OpBicgA)
+    or the update sweep + one-gather SpMV (default for n >= 2^20) -- forced
+    both ways here on a medium system; bits and iteration counts unchanged,
+    launches per iteration 1/2 (CG) and 2/3 (BiCGStab)."""
+    monkeypatch.setenv("PK_CG_SPLIT", split)
+    monkeypatch.setenv("PK_BICG_SPLIT", split)
+    a, b = pk.convdiff2d(96)
+    pa, pb = pk.poisson2d_grid(96)
+    for method, A, B in (("cg", pa, pb), ("bicgstab", a, b)):
+        for kw, okw in (({}, {}), ({"fixed_iterations": 9, "max_iterations": 9}, {"fixed": 9, "max_iterations": 9})):
+            res = pk.SOLVERS[(method, "pipelined")](A, B, config=pk.SolverConfig(**kw))
+            assert_identical(res, oracle_run(method, A, B, (128, 256), **okw))
+            want = {"cg": 1, "bicgstab": 2}[method] + (split == "1")
+            assert [p.launches for p in res.trace.iterations[:3]] == [want] * 3
+
+
 def test_reruns_bit_identical(pk):
     a, b = pk.convdiff2d(80)
     for key, solver in pk.SOLVERS.items():
@@ -119,6 +137,8 @@ def test_trace_shape_and_counts(pk):
     assert [p.launches for p in cg.trace.iterations] == [1] * 5
     assert all(p.transfers == 0 for p in cg.trace.iterations)  # device-resident loop
     bi = pk.bicgstab_pipelined(a, b, config=cfg)
+    # small system: fused bodies (n >= 2^20 splits the update off: CG 2,
+    # BiCGStab 3 -- test_split_and_fused_bodies_identical)
     assert [p.launches for p in bi.trace.iterations] == [2] * 5
     gm = pk.gmres_pipelined(a, b, config=cfg)
     assert [p.launches for p in gm.trace.iterations] == [2, 3, 4, 4, 4]
@@ -212,6 +232,7 @@ def test_c2_bicgstab_1024_fixed_bitwise(pk):
     cfg = pk.SolverConfig(fixed_iterations=8, max_iterations=8)
     res = pk.bicgstab_pipelined(dm, b, config=cfg)
     assert_identical(res, oracle_run("bicgstab", a, b, (128, 256), fixed=8, max_iterations=8))
+    assert [p.launches for p in res.trace.iterations[:2]] == [3, 3]  # split body at n = 2^20
 
 
 def test_c3_gmres_128_fixed_bitwise(pk):
