@@ -230,12 +230,18 @@ def run_workload(args, world, rank, local):
         n = side ** 3
         nnz = 7 * n - 6 * side * side
         us = loop_s / iters * 1e6
-        per_gpu = (b_csr(n, nnz) + 64 * n) / world + 3 * 2 * 8 * side * side * (world > 1)
+        # fused step: B_CSR + 64 n (x, r, p, Ap read; x, r', p', Ap' written) and
+        # 3 halo planes per neighbour; split step (partitions >= 2^20 rows):
+        # sweep 56 n + SpMV B_CSR + 24 n and 1 halo plane
+        split = int(res.diagnostics.get("launches_per_iteration", 2)) >= 3
+        halo_planes = 1 if split else 3
+        per_gpu = (b_csr(n, nnz) + (80 if split else 64) * n) / world + halo_planes * 2 * 8 * side * side * (world > 1)
         line.update({"value": round(us, 3), "ms_per_step": round(us / 1e3, 6), "scaling": "strong",
                      "config": {"workload": f"pipelined CG, 3D Poisson 7-point {side}^3 row-partitioned over {world} "
                                             f"GPU(s) (configs[3])", "n": n, "nnz": nnz,
                                 "reduction_geometry": f"{n // gs}x{gs}", "parallelism": f"row-slabs x{world}",
-                                "collectives_per_iteration": "1 allgather of group partials + halo send/recv"},
+                                "collectives_per_iteration": "1 allgather of group partials + halo send/recv",
+                                "loop_body": "update sweep + p' halo + SpMV" if split else "fused recompute-at-gather"},
                      "iteration_roofline": {"bytes_per_iteration_per_gpu": int(per_gpu),
                                             "achieved_gbs_per_gpu": round(per_gpu / (us * 1e-6) / 1e9, 1),
                                             "frac": round(per_gpu / (us * 1e-6) / 1e9 / peak, 4)},

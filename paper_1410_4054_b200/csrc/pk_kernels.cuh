@@ -519,13 +519,15 @@ struct OpCgApNext {
   double* r[2];
   double* p[2];
   double* ap[2];
+  int64_t goff;      // gather base = own base - goff (row-partitioned halo layout; 0 otherwise)
   const double* rn;
   const double* pn;
+  const double* pg;
   double* apn;
   struct Item { double r, p; };
   struct Gat { double p; };
   __device__ __forceinline__ void load(uint32_t row, Item& it) const { it.r = __ldg(rn + row); it.p = __ldg(pn + row); }
-  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const { g.p = __ldg(pn + col); }
+  __device__ __forceinline__ void gload(uint32_t col, Gat& g) const { g.p = __ldg(pg + col); }
   __device__ __forceinline__ double gval(const Gat& g) const { return g.p; }
   template <int M>
   __device__ __forceinline__ void compute(uint32_t row, Item& it, double q, double (&c)[M]) const {
@@ -537,6 +539,7 @@ struct OpCgApNext {
   __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
     const int cur = ld_par(sp.par);
     rn = cur ? r[0] : r[1]; pn = cur ? p[0] : p[1]; apn = cur ? ap[0] : ap[1];
+    pg = pn - goff;
   }
 };
 

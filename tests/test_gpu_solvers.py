@@ -281,11 +281,15 @@ def test_batch_other_drivers(pk, tag):
 # ---------------------------------------------------------------------------
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_c4_partitioned_cg_bitwise(pk, world):
+def test_c4_partitioned_cg_bitwise(pk, world, split, monkeypatch):
     """gen_poisson3d_block(32, 1) split into `world` z-slabs: halo exchange +
     one partials allgather per iteration reproduce the single-device oracle at
-    the same geometry bit for bit."""
+    the same geometry bit for bit; both loop forms (fused
+    step with r/p/Ap halos, or update sweep + p' halo + SpMV -- the default
+    for partitions >= 2^20 rows)."""
+    monkeypatch.setenv("PK_CG_SPLIT", split)
     side, gs = 32, 1024
     geom = pk.slab_geometry(side, gs)
     a, b = pk.gen_poisson3d_block(side, 1)
