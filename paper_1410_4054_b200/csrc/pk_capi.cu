@@ -94,6 +94,11 @@ struct pk_ctx {
   unsigned* ticket = nullptr;
   std::vector<pk_ctx*> workers;   // pk_solve_batch worker contexts (kept across calls)
   bool pdl = false;               // PK_PDL=1: programmatic stream serialization (measured slower, off)
+  int mat_mink = 0;               // two-phase SpMV engine for CHAIN chains K >= mat_mink (PK_MAT_MINK=9 to try; 0 = off:
+                                  // measured slower than the fused engine on C2, profiles/ENGINE_EXPERIMENTS.md)
+  double* mat = nullptr;          // its contribution buffer, mat_cap doubles
+  size_t mat_cap = 0;
+  bool mat_discard = true;        // PK_MAT_DISCARD=0: keep consumed lines in L2 (write-back on eviction)
 };
 
 struct pk_mat {
@@ -162,6 +167,139 @@ __global__ void __launch_bounds__(32, 8)
   op.scalars(sp);
   bool last = engine_warp_chain<NQ, R>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
   if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing, smem, kWarpStage2Doubles);
+}
+
+// ---------------------------------------------------------------------------
+// two-phase ("materialised") engine for SpMV operators on long lane chains
+// ---------------------------------------------------------------------------
+//
+// Phase 1 (k_mat_rows): plain grid-stride thread-per-row code -- the SpMV row,
+// the operator's vector outputs and its NQ dot contributions c_q[row], which
+// are stored to a contribution buffer cb[q][n] (coalesced).  No shared
+// memory, no barrier: full occupancy, the row code runs at streaming speed.
+// Phase 2 (k_mat_fold): thread = lane t of [0, G); it folds its chain
+// cb[q][t], cb[q][t+G], ... serially in chunk order (linalg.py:300-303;
+// rows past n add +0.0, which cannot change a sum that starts at +0.0), with
+// UF chunks x NQ quantities of loads in flight; a warp's loads are 32
+// consecutive doubles.  Lane values go to the spill buffer, the CTA that
+// completes a group runs its halving tree (group_tree, linalg.py:304-307),
+// the CTA completing the last group runs the finalizer.
+// The buffer (8 B x nq x n) is written and read back within two launches and
+// mostly served by L2.  Same IEEE operations on the same operands, in the
+// same order, as the fused engine: bit-identical partials.
+template <int NQ, class Op>
+__global__ void __launch_bounds__(256, 4)
+    k_mat_rows(int64_t n, const __grid_constant__ Op op0, ScalarPtrs sp, double* __restrict__ cb, int nstore,
+               SolveState* st, int gate, const int32_t* skip) {
+  pdl_wait();
+  pdl_trigger();
+  if (skip && *(volatile const int32_t*)skip) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  if (st && !gate_open(st, gate, ing)) return;
+  Op op = op0;
+  op.scalars(sp);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += stride) {
+    double c[NQ];
+    row_contrib<NQ>(op, (uint32_t)row, c);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (q < nstore) cb[(int64_t)q * n + row] = c[q];
+  }
+}
+
+// quantities of one lane chain are folded by NQP (power of two >= NQ)
+// different threads: a CTA covers kMatLanes(NQ) = 256 / NQP lanes
+__host__ __device__ constexpr int mat_nqp(int nq) { return nq <= 1 ? 1 : nq <= 2 ? 2 : 4; }
+__host__ __device__ constexpr int mat_lanes(int nq) { return kThreads / mat_nqp(nq); }
+
+template <int NQ>
+__global__ void __launch_bounds__(kThreads, 4)
+    k_mat_fold(const __grid_constant__ Geom geo, const double* __restrict__ cb, double* part, int ld, int col0,
+               int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin, int fin_arg,
+               int smem_d, int discard) {
+  extern __shared__ double smem[];
+  __shared__ int s_flag;
+  __shared__ int s_last;
+  pdl_wait();
+  pdl_trigger();
+  if (skip && *(volatile const int32_t*)skip) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  if (st && !gate_open(st, gate, ing)) return;
+  constexpr int LPB = mat_lanes(NQ);
+  const int tid = threadIdx.x;
+  const int q = tid / LPB;  // the quantity this thread folds
+  const int64_t n = geo.n, G = geo.G, K = geo.K;
+  const int64_t lid0 = (int64_t)blockIdx.x * LPB;
+  const int nl = (int)((G - lid0) < LPB ? (G - lid0) : LPB);
+  const int64_t l = lid0 + tid % LPB;
+  if (tid == 0) s_last = 0;
+  if (tid % LPB < nl && q < nstore) {
+    // full rounds (every row < n): UF loads issued back to back (volatile
+    // asm keeps them together), then the ordered adds
+    constexpr int UF = 16;
+    double acc = 0.0;
+    const double* pq = cb + (int64_t)q * n + l;
+    const int64_t Kf = n / G;  // chunks whose rows are all < n
+    int64_t k = 0;
+    for (; k + UF <= Kf; k += UF) {
+      double v[UF];
+#pragma unroll
+      for (int u = 0; u < UF; ++u) asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v[u]) : "l"(pq + (k + u) * G));
+#pragma unroll
+      for (int u = 0; u < UF; ++u) acc = add_rn(acc, v[u]);
+      if (discard) {
+        // the lines just consumed are dead: drop them from L2 without a
+        // write-back (lane 16 j owns the 128-B line of lanes 16 j .. 16 j + 15)
+        __syncwarp();
+        if ((l & 15) == 0) {
+#pragma unroll
+          for (int u = 0; u < UF; ++u) asm volatile("discard.global.L2 [%0], 128;" ::"l"(pq + (k + u) * G) : "memory");
+        }
+      }
+    }
+    for (; k < K; ++k) acc = add_rn(acc, k * G + l < n ? __ldg(pq + k * G) : 0.0);
+    scr.spill[(int64_t)q * G + l] = acc;
+  }
+  __syncthreads();
+  int ncomplete = 0;
+  double* tail = smem;
+  if (geo.gs >= LPB) {
+    const int g = (int)(lid0 / geo.gs);
+    if (tid == 0) {
+      const unsigned per = (unsigned)(geo.gs / LPB);
+      unsigned tk = atomic_add_release(scr.gtick + g, 1u);
+      int last = (tk == per - 1);
+      if (last) scr.gtick[g] = 0u;
+      s_flag = last;
+    }
+    __syncthreads();
+    if (s_flag) {
+      group_tree<NQ>(geo, g, scr.spill, tail, part, ld, col0, nstore);
+      ncomplete = 1;
+    }
+  } else {
+    const int g0 = (int)(lid0 / geo.gs);
+    int g1 = (int)((lid0 + nl + geo.gs - 1) / geo.gs);
+    if (g1 > geo.n_groups) g1 = geo.n_groups;
+    for (int g = g0; g < g1; ++g) group_tree<NQ>(geo, g, scr.spill, tail, part, ld, col0, nstore);
+    ncomplete = g1 - g0;
+  }
+  if (ncomplete > 0) {
+    __syncthreads();
+    if (tid == 0) {
+      unsigned* ticket = st ? &st->ticket : scr.ticket;
+      unsigned tk = atomic_add_release(ticket, (unsigned)ncomplete);
+      if (tk + (unsigned)ncomplete == (unsigned)geo.n_groups) {
+        *ticket = 0u;
+        s_last = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_last && fin != FIN_NONE && st && tid < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
 }
 
 template <class Op>
@@ -345,8 +483,30 @@ __global__ void k_row_max(const int64_t* counts, int64_t n, unsigned long long* 
 // quantities.  Must be called outside stream capture (it may reallocate).
 static int64_t min_units(const pk_ctx* c) { return (int64_t)c->sm_count * 4; }
 
+static bool mat_applies(const pk_ctx* c, const Geom& geo) {
+  return c->mat_mink > 0 && !geo.leaf && geo.K >= c->mat_mink;
+}
+
+// L2 discard of consumed contribution lines: only when every warp's 32-lane
+// segment is whole 128-B lines (n and G multiples of 32)
+static int mat_discard(const pk_ctx* c, const Geom& geo) {
+  return c->mat_discard && geo.n % 32 == 0 && geo.G % 32 == 0 ? 1 : 0;
+}
+
 static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
   Geom geo = make_geom(n, c->ng, c->gs, min_units(c));
+  if (mat_applies(c, geo)) {
+    // SpMV operators carry at most 4 quantities
+    const size_t mneed = (size_t)n * (size_t)std::min(std::max(nq, 1), 4);
+    if (mneed > c->mat_cap) {
+      PK_CUDA(cudaStreamSynchronize(c->stream));
+      if (c->mat) cudaFree(c->mat);
+      c->mat = nullptr;
+      c->mat_cap = 0;
+      PK_CUDA(cudaMalloc(&c->mat, mneed * sizeof(double)));
+      c->mat_cap = mneed;
+    }
+  }
   if (geo.leaf && geo.logf == 0) return PK_OK;
   size_t need = geo.leaf ? (size_t)geo.units * 32 * (size_t)std::max(nq, 1) : (size_t)geo.G * (size_t)std::max(nq, 1);
   if (need <= c->spill_cap) return PK_OK;
@@ -411,6 +571,22 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
     return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
   if (geo.leaf && geo.logf > 0 && (size_t)geo.units * 32 * NQ > c->spill_cap)
     return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
+  if constexpr (Op::kSpmv && NQ <= 4) {
+    if (mat_applies(c, geo) && c->mat_cap >= (size_t)n * (size_t)nstore) {
+      auto kr = k_mat_rows<NQ, Op>;
+      cudaError_t e = launch_k(c->pdl, kr, dim3(engine_grid(c, kr, 0, (n + 255) / 256, 256)), dim3(256), 0, s, n,
+                               op, sp, c->mat, nstore, st, gate, skip);
+      if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("two-phase rows launch: ") + cudaGetErrorString(e));
+      const int fd = (int)std::max<size_t>(engine_tail_doubles(geo, NQ), 1024);
+      auto kf = k_mat_fold<NQ>;
+      PK_TRY(allow_dynamic_smem(kf, (size_t)fd * sizeof(double)));
+      e = launch_k(c->pdl, kf, dim3((unsigned)((geo.G + mat_lanes(NQ) - 1) / mat_lanes(NQ))), dim3(kThreads),
+                   (size_t)fd * sizeof(double), s, geo, (const double*)c->mat, part, ld, col0, nstore, scratch_of(c),
+                   st, gate, skip, fin, fin_arg, fd, mat_discard(c, geo));
+      if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("two-phase fold launch: ") + cudaGetErrorString(e));
+      return PK_OK;
+    }
+  }
   if constexpr (NQ <= 4) {
   if (!geo.leaf && geo.gs >= 32 && geo.K >= 2 && geo.K <= 8) {
     // warp-per-unit chain engine (no shared staging, no CTA barrier): wins
@@ -653,6 +829,8 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   }
   c->stream = c->own;
   if (const char* e2 = getenv("PK_PDL")) c->pdl = atoi(e2) != 0;
+  if (const char* e3 = getenv("PK_MAT_MINK")) c->mat_mink = atoi(e3);
+  if (const char* e4 = getenv("PK_MAT_DISCARD")) c->mat_discard = atoi(e4) != 0;
   // keep freed workspace memory in the stream-ordered pool between solves
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -674,6 +852,7 @@ extern "C" int pk_ctx_destroy(pk_ctx* c) {
   if (c->scratch_d) cudaFree(c->scratch_d);
   if (c->gtick) cudaFree(c->gtick);
   if (c->spill) cudaFree(c->spill);
+  if (c->mat) cudaFree(c->mat);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return PK_OK;

@@ -119,6 +119,23 @@ def test_split_and_fused_bodies_identical(pk, split, monkeypatch):
             assert [p.launches for p in res.trace.iterations[:3]] == [want] * 3
 
 
+@pytest.mark.parametrize("geom", [(8, 64), (4, 32), (2, 512)])
+def test_two_phase_engine_identical(pk, geom, monkeypatch):
+    """Two-phase SpMV engine (opt-in, PK_MAT_MINK read at context creation):
+    thread-per-row pass storing the contributions, then the ordered lane-chain
+    fold.  Geometries cover a group spanning several fold CTAs (2 x 512),
+    one (8 x 64) and several groups per fold CTA (4 x 32); chains K >= 9.
+    Bits, iteration counts and termination identical to the oracle."""
+    monkeypatch.setenv("PK_MAT_MINK", "9")
+    a, b = pk.convdiff2d(96)
+    pa, pb = pk.poisson2d_grid(96)
+    ctx = pk.ExecutionContext(*geom, device=0)
+    for method, A, B in (("cg", pa, pb), ("bicgstab", a, b), ("gmres", a, b)):
+        for kw, okw in (({}, {}), ({"fixed_iterations": 9, "max_iterations": 9}, {"fixed": 9, "max_iterations": 9})):
+            res = pk.SOLVERS[(method, "pipelined")](A, B, config=pk.SolverConfig(**kw), context=ctx)
+            assert_identical(res, oracle_run(method, A, B, geom, **okw))
+
+
 def test_reruns_bit_identical(pk):
     a, b = pk.convdiff2d(80)
     for key, solver in pk.SOLVERS.items():
