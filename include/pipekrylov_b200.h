@@ -180,6 +180,28 @@ int pk_reduce_stage1(pk_ctx* ctx, int64_t n, int32_t nq, const double* const* co
 int pk_reduce_stage2(pk_ctx* ctx, int32_t nq, const double* partials, double* totals);
 /* dot (linalg.py:351-365): total written to device *total. */
 int pk_dot(pk_ctx* ctx, int64_t n, const double* x, const double* y, double* total);
+/* Classical-driver vector updates, one launch each (linalg.py:403-457,
+ * solvers.py:277-280, 477-482), IEEE mul/add with no contraction, in the
+ * NumPy expression order of the reference:
+ *   PK_VEC_AXPY        y = y + (alpha x)                     axpy
+ *   PK_VEC_AXPY2       y = y + ((alpha x) + (beta z))        axpy2
+ *   PK_VEC_XPAY        y = (y beta) + x                      xpay
+ *   PK_VEC_SCALE       y = y alpha                           scale
+ *   PK_VEC_ADD_SCALED  y = x + (alpha z)    (y a fresh output) add_scaled
+ *   PK_VEC_BICG_P      y = ((y - (beta z)) alpha) + x        _bicgstab_p_update
+ *   PK_VEC_COPY        y = x                                 _device_copy
+ * Unused vector arguments may be NULL. */
+enum {
+  PK_VEC_AXPY = 0,
+  PK_VEC_AXPY2 = 1,
+  PK_VEC_XPAY = 2,
+  PK_VEC_SCALE = 3,
+  PK_VEC_ADD_SCALED = 4,
+  PK_VEC_BICG_P = 5,
+  PK_VEC_COPY = 6
+};
+int pk_vec_update(pk_ctx* ctx, int32_t kind, int64_t n, double* y, const double* x, const double* z,
+                  double alpha, double beta);
 /* fused_cg_vector_update (fused.py:123-151). */
 int pk_cg_update(pk_ctx* ctx, int64_t n, double* x, double* r, double* p, const double* ap,
                  double alpha, double beta, double* partials);

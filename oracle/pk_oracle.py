@@ -473,6 +473,220 @@ SOLVERS = {"cg": cg_pipelined, "bicgstab": bicgstab_pipelined, "gmres": gmres_pi
 
 
 # ---------------------------------------------------------------------------
+# classical drivers (solvers.py:310-389, 485-580, 725-858): one BLAS op per
+# step, scalars on the host.  NumPy expression order of linalg.py:403-457.
+# ---------------------------------------------------------------------------
+
+
+def cg_classical(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None,
+                 geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL, timing=None):
+    """Restatement of solvers.cg_classical (solvers.py:310-389)."""
+    a, b, x = _setup(a, b, x0)
+    lbt = 0.0 if fixed else btol
+    limit = fixed if fixed else max_iterations
+    norm_b = math.sqrt(dot(b, b, geom))
+    scale = norm_b if norm_b > 0 else 1.0
+    r = b + (-1.0) * csr_spmv(a, x)  # add_scaled (linalg.py:451-457)
+    p = r.copy()
+    rr = dot(r, r, geom)
+    hist = []
+    term, kind = MAX_ITER, None
+    if math.sqrt(rr) / scale <= tol and (not fixed or rr == 0.0):
+        return _finish(a, b, x, geom, hist, CONVERGED, None)
+    t0 = time.perf_counter()
+    for _ in range(limit):
+        q = csr_spmv(a, p)
+        pap = dot(p, q, geom)
+        if abs(pap) < lbt or pap == 0.0:  # pap == 0: ZeroDivisionError in the reference
+            term, kind = BREAKDOWN, "pAp"
+            break
+        alpha = rr / pap
+        x += alpha * p  # axpy (linalg.py:403-411)
+        r += (-alpha) * q
+        rr_new = dot(r, r, geom)
+        mon = math.sqrt(rr_new) / scale
+        hist.append(mon)
+        if not math.isfinite(mon):
+            term, kind = BREAKDOWN, "divergence"
+            break
+        if not fixed and mon <= tol:
+            term = CONVERGED
+            break
+        beta = rr_new / rr
+        p *= beta  # xpay (linalg.py:428-438): y *= beta; y += x
+        p += r
+        rr = rr_new
+    if timing is not None:
+        timing["loop_seconds"] = time.perf_counter() - t0
+    return _finish(a, b, x, geom, hist, term, kind)
+
+
+def bicgstab_classical(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None,
+                       geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL, timing=None):
+    """Restatement of solvers.bicgstab_classical (solvers.py:485-580)."""
+    a, b, x = _setup(a, b, x0)
+    lbt = 0.0 if fixed else btol
+    limit = fixed if fixed else max_iterations
+    norm_b = math.sqrt(dot(b, b, geom))
+    scale = norm_b if norm_b > 0 else 1.0
+    r = b + (-1.0) * csr_spmv(a, x)
+    r0s = r.copy()
+    p = r.copy()
+    rr = dot(r, r, geom)
+    rho = dot(r, r0s, geom)
+    hist = []
+    term, kind = MAX_ITER, None
+    if math.sqrt(rr) / scale <= tol and (not fixed or rr == 0.0):
+        return _finish(a, b, x, geom, hist, CONVERGED, None)
+    t0 = time.perf_counter()
+    for _ in range(limit):
+        ap = csr_spmv(a, p)
+        apr = dot(ap, r0s, geom)
+        if abs(apr) < lbt or apr == 0.0:
+            term, kind = BREAKDOWN, "Apr0star"
+            break
+        alpha = rho / apr
+        s = r + (-alpha) * ap
+        ss = dot(s, s, geom)
+        mon_s = math.sqrt(ss) / scale
+        if not fixed and mon_s <= tol:
+            x += alpha * p
+            hist.append(mon_s)
+            term = CONVERGED
+            break
+        as_ = csr_spmv(a, s)
+        ass = dot(as_, s, geom)
+        asas = dot(as_, as_, geom)
+        asr = dot(as_, r0s, geom)
+        if asas < lbt or asas == 0.0:
+            term, kind = BREAKDOWN, "AsAs"
+            break
+        omega = ass / asas
+        x += alpha * p + omega * s  # axpy2 (linalg.py:414-425)
+        r = s + (-omega) * as_
+        rho_new = dot(r, r0s, geom)
+        rr = dot(r, r, geom)
+        mon = math.sqrt(rr) / scale
+        hist.append(mon)
+        if not math.isfinite(mon):
+            term, kind = BREAKDOWN, "divergence"
+            break
+        if not fixed and mon <= tol:
+            term = CONVERGED
+            break
+        if abs(rho_new) < lbt:
+            term, kind = BREAKDOWN, "rho"
+            break
+        if abs(omega) < lbt:
+            term, kind = BREAKDOWN, "omega"
+            break
+        beta = -asr / apr
+        p -= omega * ap  # _bicgstab_p_update (solvers.py:477-482)
+        p *= beta
+        p += r
+        rho = rho_new
+    if timing is not None:
+        timing["loop_seconds"] = time.perf_counter() - t0
+    return _finish(a, b, x, geom, hist, term, kind)
+
+
+def gmres_classical(a, b, x0=None, tol=1e-8, max_iterations=500, fixed=None, restart=30, mgs=False,
+                    geom=(DEFAULT_N_GROUPS, DEFAULT_GROUP_SIZE), btol=DEFAULT_BTOL, timing=None):
+    """Restatement of solvers.gmres_classical (solvers.py:725-858), CGS
+    (solvers.py:240-251) or MGS (solvers.py:221-237)."""
+    a, b, x = _setup(a, b, x0)
+    lbt = 0.0 if fixed else btol
+    limit = fixed if fixed else max_iterations
+    m = restart
+    hist = []
+    term, kind = MAX_ITER, None
+    total = 0
+    norm_b = None
+    scale = 1.0
+    done = False
+    while not done and total < limit:
+        if norm_b is None:
+            norm_b = math.sqrt(dot(b, b, geom))
+            scale = norm_b if norm_b > 0 else 1.0
+        r = b + (-1.0) * csr_spmv(a, x)
+        rho = math.sqrt(dot(r, r, geom))
+        start_ok = rho > 0 and not (not fixed and rho / scale <= tol)
+        if not start_ok:
+            term = CONVERGED
+            break
+        r *= 1.0 / rho  # scale (linalg.py:441-448)
+        basis, xi = [], []
+        rmat = np.zeros((m, m))
+        est2 = 1.0
+        lucky = conv = False
+        t0 = time.perf_counter()
+        while len(basis) < m and total < limit:
+            i = len(basis) + 1
+            w = csr_spmv(a, basis[-1] if basis else r)
+            coeffs = np.zeros(len(basis))
+            if mgs:
+                for j, q in enumerate(basis):
+                    coeffs[j] = dot(q, w, geom)
+                    w += (-coeffs[j]) * q
+            else:
+                for j, q in enumerate(basis):
+                    coeffs[j] = dot(q, w, geom)
+                for j, q in enumerate(basis):
+                    w += (-coeffs[j]) * q
+            for j, c in enumerate(coeffs):
+                rmat[j, i - 1] = float(c)
+            nrm = math.sqrt(dot(w, w, geom))
+            if nrm < lbt or nrm == 0.0:
+                lucky = True
+                break
+            rmat[i - 1, i - 1] = nrm
+            w *= 1.0 / nrm
+            basis.append(w)
+            xi_i = dot(r, w, geom)
+            xi.append(xi_i)
+            r += (-xi_i) * w
+            est2 = max(est2 - xi_i * xi_i, 0.0)
+            mon = rho * math.sqrt(est2) / scale
+            hist.append(mon)
+            total += 1
+            if not math.isfinite(mon):
+                term, kind, done = BREAKDOWN, "divergence", True
+                break
+            if not fixed and mon <= tol:
+                conv = True
+                break
+        if timing is not None:
+            timing["loop_seconds"] = timing.get("loop_seconds", 0.0) + time.perf_counter() - t0
+        k = len(basis)
+        gate = None
+        if k > 0 and term != BREAKDOWN:
+            try:
+                eta = solve_upper_triangular(rmat[:k, :k], np.asarray(xi), btol)
+            except Breakdown as e:
+                term, kind, done, eta = BREAKDOWN, e.kind, True, None
+            if eta is not None:
+                upd = eta[0] * r
+                for idx in range(1, k + 1):
+                    coeff = (eta[idx] if idx < k else 0.0) + eta[0] * xi[idx - 1]
+                    upd += coeff * basis[idx - 1]
+                x += rho * upd
+                if conv or lucky:
+                    gate = _true_residual(a, b, x, geom)
+        if term == BREAKDOWN:
+            pass
+        elif conv or lucky:
+            if gate is not None and gate <= tol * scale:
+                term, done = CONVERGED, True
+            elif lucky and k == 0:
+                term, done = LUCKY_BREAKDOWN, True
+    return _finish(a, b, x, geom, hist, term, kind)
+
+
+CLASSICAL = {"cg": cg_classical, "bicgstab": bicgstab_classical, "gmres": gmres_classical}
+
+
+
+# ---------------------------------------------------------------------------
 # generators (io.py:201-275 for the Poisson families; convection-diffusion
 # families are defined by this project, see DESIGN.md "Inputs")
 # ---------------------------------------------------------------------------

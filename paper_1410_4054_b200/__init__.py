@@ -47,13 +47,24 @@ from .solvers import (
     solve_upper_triangular,
 )
 
+from .classical import bicgstab_classical, cg_classical, gmres_classical, orthogonalize_mgs  # noqa: E402
+
+# the reference's classical drivers (solvers.py:310-389, 485-580, 725-858) on
+# the same B200 kernels: SOLVERS[(method, "classical")], as in the reference
+SOLVERS.update({
+    ("cg", "classical"): cg_classical,
+    ("bicgstab", "classical"): bicgstab_classical,
+    ("gmres", "classical"): gmres_classical,
+})
+
 __version__ = "0.1.0"
 
 __all__ = [
     "BREAKDOWN", "CLASSICAL_GS", "CONVERGED", "DEFAULT_BREAKDOWN_TOLERANCE", "DEFAULT_CONTEXT",
     "LUCKY_BREAKDOWN", "MAX_ITER", "MODIFIED_GS", "PartitionedCG", "SOLVERS", "BreakdownError", "CsrMatrix",
     "DeviceContext", "DeviceMatrix", "ExecutionContext", "ExecutionTrace", "PhaseRecord", "SolverConfig",
-    "SolverResult", "UpperTriangular", "WorkgroupPartials", "as_vector", "bicgstab_pipelined",
+    "SolverResult", "UpperTriangular", "WorkgroupPartials", "as_vector", "bicgstab_classical", "bicgstab_pipelined",
+    "cg_classical", "gmres_classical", "orthogonalize_mgs",
     "cg_partitioned", "cg_pipelined", "context_for", "convdiff2d", "convdiff3d", "device_matrix", "gen_poisson2d",
     "gen_poisson3d_block", "gmres_pipelined", "poisson2d_grid", "poisson3d_grid", "solve", "solve_batch",
     "slab_geometry", "solve_upper_triangular", "__version__",

@@ -21,6 +21,8 @@ TERM_NAMES = {0: "converged", 1: "max_iter", 2: "breakdown", 3: "lucky_breakdown
 KIND_NAMES = {0: None, 1: "pAp", 2: "Apr0star", 3: "AsAs", 4: "divergence", 5: "singular_R"}
 METHODS = {"cg": 0, "bicgstab": 1, "gmres": 2}
 DOT_INPUT, DOT_RESULT, DOT_VECTOR = 0, 1, 2
+# pk_vec_update kinds (include/pipekrylov_b200.h PK_VEC_*)
+VEC_AXPY, VEC_AXPY2, VEC_XPAY, VEC_SCALE, VEC_ADD_SCALED, VEC_BICG_P, VEC_COPY = range(7)
 GEN = {"poisson2d": 0, "poisson3d": 1, "convdiff2d": 2, "convdiff3d": 3}
 LOOP_GRAPH, LOOP_HOST = 0, 1
 FLAG_PROFILE = 1
@@ -92,6 +94,7 @@ SIGNATURES = {
     "pk_reduce_stage1": [_P, C.c_int64, C.c_int32, C.POINTER(_P), _P],
     "pk_reduce_stage2": [_P, C.c_int32, _P, _P],
     "pk_dot": [_P, C.c_int64, _P, _P, _P],
+    "pk_vec_update": [_P, C.c_int32, C.c_int64, _P, _P, _P, C.c_double, C.c_double],
     "pk_cg_update": [_P, C.c_int64, _P, _P, _P, _P, C.c_double, C.c_double, _P],
     "pk_bicg_s_update": [_P, C.c_int64, _P, _P, _P, _P, C.c_double, _P, _P, _P, _P],
     "pk_bicg_xrp_update": [_P, C.c_int64, _P, _P, _P, _P, _P, _P, C.c_double, C.c_double, C.c_double, _P, _P],

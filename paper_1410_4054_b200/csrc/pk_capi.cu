@@ -1182,6 +1182,51 @@ extern "C" int pk_reduce_stage2(pk_ctx* c, int32_t nq, const double* partials, d
   return PK_OK;
 }
 
+// Classical-driver BLAS-1 updates (linalg.py:403-457): one grid-stride
+// elementwise kernel, V elements per thread in flight, the NumPy expression
+// order with explicit round-to-nearest operations.
+template <int KIND>
+__global__ void __launch_bounds__(256) k_vec_update(int64_t n, double* __restrict__ y, const double* __restrict__ x,
+                                                    const double* __restrict__ z, double alpha, double beta) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double out;
+    if constexpr (KIND == PK_VEC_AXPY) out = add_rn(y[i], mul_rn(alpha, x[i]));
+    else if constexpr (KIND == PK_VEC_AXPY2) out = add_rn(y[i], add_rn(mul_rn(alpha, x[i]), mul_rn(beta, z[i])));
+    else if constexpr (KIND == PK_VEC_XPAY) out = add_rn(mul_rn(y[i], beta), x[i]);
+    else if constexpr (KIND == PK_VEC_SCALE) out = mul_rn(y[i], alpha);
+    else if constexpr (KIND == PK_VEC_ADD_SCALED) out = add_rn(x[i], mul_rn(alpha, z[i]));
+    else if constexpr (KIND == PK_VEC_BICG_P) out = add_rn(mul_rn(sub_rn(y[i], mul_rn(beta, z[i])), alpha), x[i]);
+    else out = x[i];
+    y[i] = out;
+  }
+}
+
+extern "C" int pk_vec_update(pk_ctx* c, int32_t kind, int64_t n, double* y, const double* x, const double* z,
+                             double alpha, double beta) {
+  PK_CHECK_CTX(c);
+  if (n < 0 || (n > 0 && !y)) return fail(PK_ERR_INVALID, "bad argument");
+  const bool need_x = kind == PK_VEC_AXPY || kind == PK_VEC_AXPY2 || kind == PK_VEC_XPAY ||
+                      kind == PK_VEC_ADD_SCALED || kind == PK_VEC_BICG_P || kind == PK_VEC_COPY;
+  const bool need_z = kind == PK_VEC_AXPY2 || kind == PK_VEC_ADD_SCALED || kind == PK_VEC_BICG_P;
+  if (kind < PK_VEC_AXPY || kind > PK_VEC_COPY) return fail(PK_ERR_INVALID, "unknown vector update kind");
+  if (n > 0 && ((need_x && !x) || (need_z && !z))) return fail(PK_ERR_INVALID, "missing vector argument");
+  if (n == 0) return PK_OK;
+  const dim3 grid((unsigned)grid_elem(c, n, 256)), block(256);
+  cudaStream_t s = c->stream;
+  switch (kind) {
+    case PK_VEC_AXPY: k_vec_update<PK_VEC_AXPY><<<grid, block, 0, s>>>(n, y, x, z, alpha, beta); break;
+    case PK_VEC_AXPY2: k_vec_update<PK_VEC_AXPY2><<<grid, block, 0, s>>>(n, y, x, z, alpha, beta); break;
+    case PK_VEC_XPAY: k_vec_update<PK_VEC_XPAY><<<grid, block, 0, s>>>(n, y, x, z, alpha, beta); break;
+    case PK_VEC_SCALE: k_vec_update<PK_VEC_SCALE><<<grid, block, 0, s>>>(n, y, x, z, alpha, beta); break;
+    case PK_VEC_ADD_SCALED: k_vec_update<PK_VEC_ADD_SCALED><<<grid, block, 0, s>>>(n, y, x, z, alpha, beta); break;
+    case PK_VEC_BICG_P: k_vec_update<PK_VEC_BICG_P><<<grid, block, 0, s>>>(n, y, x, z, alpha, beta); break;
+    default: k_vec_update<PK_VEC_COPY><<<grid, block, 0, s>>>(n, y, x, z, alpha, beta); break;
+  }
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}
+
 extern "C" int pk_dot(pk_ctx* c, int64_t n, const double* x, const double* y, double* total) {
   PK_CHECK_CTX(c);
   if (!total || n < 0) return fail(PK_ERR_INVALID, "bad argument");

@@ -5,8 +5,10 @@ Run in the development container (where /root/reference exists):
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
 
-Writes tests/golden/fused_golden.npz, tests/golden/solver_golden.npz and
-tests/golden/manifest.json.  The fixtures pin the oracle (oracle/pk_oracle.py)
+Writes tests/golden/fused_golden.npz, tests/golden/solver_golden.npz,
+tests/golden/classical_golden.npz and tests/golden/manifest.json
+(``--classical``: only the classical-driver fixtures, merged into the
+existing manifest).  The fixtures pin the oracle (oracle/pk_oracle.py)
 and, transitively, the CUDA path.  Inputs are stored alongside outputs so the
 GPU box (which has no reference and may have different RNG streams) replays
 exactly the same problems.
@@ -134,7 +136,52 @@ def solver_cases():
     return cases
 
 
+def classical_cases():
+    """The solver cases again through the reference's CLASSICAL drivers
+    (solvers.py:310-389, 485-580, 725-858), plus modified Gram-Schmidt GMRES."""
+    cases = [c for c in solver_cases() if "x0" in c[0] or "_p1" in c[0] or "_p2" in c[0] or "zero" in c[0]
+             or "eye" in c[0] or "singular" in c[0] or "random" in c[0] or "cd2" in c[0] or "cd3" in c[0]
+             or "2x2" in c[0]]
+    p2, b2 = pk.gen_poisson2d(2)
+    cd2 = to_ref(orc.convdiff2d(24)[0])
+    cases += [
+        ("gmres_p2_mgs", "gmres", p2, b2, None, {"orthogonalization": "modified_gs"}, (128, 256)),
+        ("gmres_cd2_mgs_m7", "gmres", cd2, np.ones(cd2.n_rows), None,
+         {"orthogonalization": "modified_gs", "restart": 7, "max_iterations": 150}, (16, 32)),
+    ]
+    return cases
+
+
+def write_classical(manifest):
+    store = {}
+    manifest["classical_cases"] = []
+    for name, method, a, b, x0, cfg, geom in classical_cases():
+        fn = pk.SOLVERS[(method, "classical")]
+        ctx = pk.ExecutionContext(n_groups=geom[0], group_size=geom[1])
+        res = fn(a, b, x0=x0, config=pk.SolverConfig(**cfg), context=ctx)
+        put_csr(store, f"{name}/A", a)
+        store[f"{name}/b"] = np.asarray(b, dtype=np.float64)
+        if x0 is not None:
+            store[f"{name}/x0"] = np.asarray(x0, dtype=np.float64)
+        store[f"{name}/x"] = res.x
+        store[f"{name}/history"] = np.asarray(res.residual_history, dtype=np.float64)
+        store[f"{name}/true_final_residual"] = np.array([res.true_final_residual])
+        manifest["classical_cases"].append({
+            "name": name, "method": method, "config": cfg, "geom": list(geom),
+            "has_x0": x0 is not None, "iterations": res.iterations,
+            "termination": res.termination, "breakdown_kind": res.breakdown_kind,
+        })
+        print(f"classical {name:24s} {res.termination:16s} it={res.iterations}")
+    np.savez_compressed(HERE / "classical_golden.npz", **store)
+
+
 def main():
+    if "--classical" in sys.argv:
+        # add the classical-driver fixtures without touching the others
+        manifest = json.loads((HERE / "manifest.json").read_text())
+        write_classical(manifest)
+        (HERE / "manifest.json").write_text(json.dumps(manifest, indent=1))
+        return
     fused, manifest = {}, {}
     fused_cases(fused, manifest)
     np.savez_compressed(HERE / "fused_golden.npz", **fused)
@@ -160,6 +207,7 @@ def main():
         })
         print(f"{name:24s} {res.termination:16s} it={res.iterations}")
     np.savez_compressed(HERE / "solver_golden.npz", **solvers)
+    write_classical(manifest)
     manifest["reference"] = {"package": "pipekrylov", "version": pk.__version__,
                              "numpy": np.__version__}
     (HERE / "manifest.json").write_text(json.dumps(manifest, indent=1))

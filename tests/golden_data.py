@@ -40,3 +40,19 @@ def solver_case(name):
 
 def solver_case_names():
     return [c["name"] for c in manifest()["solver_cases"]]
+
+
+@lru_cache(maxsize=None)
+def classical():
+    return dict(np.load(GOLDEN / "classical_golden.npz"))
+
+
+def classical_case(name):
+    for case in manifest()["classical_cases"]:
+        if case["name"] == name:
+            return case
+    raise KeyError(name)
+
+
+def classical_case_names():
+    return [c["name"] for c in manifest()["classical_cases"]]

@@ -68,6 +68,39 @@ def oracle_run(method, a, b, geom, **kw):
     return orc.SOLVERS[method](a, b, geom=geom, **kw)
 
 
+@pytest.mark.parametrize("name", gd.classical_case_names())
+def test_classical_matches_reference_golden(pk, name):
+    """SOLVERS[(m, "classical")] on the B200 kernels (pk_spmv / pk_dot /
+    pk_vec_update) vs the reference's classical drivers, bitwise."""
+    case = gd.classical_case(name)
+    store = gd.classical()
+    a = pk.CsrMatrix(*gd.csr_arrays(store, f"{name}/A"))
+    b = store[f"{name}/b"]
+    x0 = store.get(f"{name}/x0")
+    cfg = pk.SolverConfig(**case["config"])
+    ctx = pk.ExecutionContext(*case["geom"])
+    res = pk.SOLVERS[(case["method"], "classical")](a, b, x0=x0, config=cfg, context=ctx)
+    ref = {"iterations": case["iterations"], "termination": case["termination"],
+           "breakdown_kind": case["breakdown_kind"], "history": store[f"{name}/history"],
+           "x": store[f"{name}/x"], "true_final_residual": store[f"{name}/true_final_residual"][0]}
+    assert_identical(res, ref)
+
+
+@pytest.mark.parametrize("method", ["cg", "bicgstab", "gmres"])
+def test_classical_matches_oracle_medium(pk, method):
+    """Classical drivers on a 120^2 system vs the oracle's classical
+    restatement at two geometries (incl. MGS for GMRES)."""
+    a, _ = pk.convdiff2d(120) if method != "cg" else pk.poisson2d_grid(120)
+    b = np.random.default_rng(2).random(a.n_rows)
+    for geom in ((128, 256), (16, 1024)):
+        for mgs in ((False, True) if method == "gmres" else (False,)):
+            kw = {"orthogonalization": "modified_gs"} if mgs else {}
+            res = pk.SOLVERS[(method, "classical")](a, b, config=pk.SolverConfig(max_iterations=200, **kw),
+                                                     context=pk.ExecutionContext(*geom))
+            okw = {"mgs": mgs} if method == "gmres" else {}
+            assert_identical(res, orc.CLASSICAL[method](a, b, geom=geom, max_iterations=200, **okw))
+
+
 @pytest.mark.parametrize("method", ["cg", "bicgstab", "gmres"])
 @pytest.mark.parametrize("geom", [(128, 256), (32, 1024), (1, 4096), (16, 65536), (1000, 64)])
 def test_solver_matches_oracle_medium(pk, method, geom):

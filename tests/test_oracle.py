@@ -93,6 +93,35 @@ def test_solver_matches_golden(name):
     assert res["true_final_residual"] == store[f"{name}/true_final_residual"][0]
 
 
+def run_oracle_classical(case, store):
+    name = case["name"]
+    a = orc.Csr(*gd.csr_arrays(store, f"{name}/A"))
+    b = store[f"{name}/b"]
+    x0 = store.get(f"{name}/x0")
+    cfg = case["config"]
+    kw = dict(tol=cfg.get("tolerance", 1e-8), max_iterations=cfg.get("max_iterations", 500),
+              fixed=cfg.get("fixed_iterations"), geom=tuple(case["geom"]))
+    if case["method"] == "gmres":
+        kw["restart"] = cfg.get("restart", 30)
+        kw["mgs"] = cfg.get("orthogonalization") == "modified_gs"
+    return orc.CLASSICAL[case["method"]](a, b, x0=x0, **kw)
+
+
+@pytest.mark.parametrize("name", gd.classical_case_names())
+def test_classical_matches_golden(name):
+    """The oracle's classical drivers (solvers.py:310-389, 485-580, 725-858)
+    reproduce the reference's own classical runs bitwise."""
+    case = gd.classical_case(name)
+    store = gd.classical()
+    res = run_oracle_classical(case, store)
+    assert res["iterations"] == case["iterations"]
+    assert res["termination"] == case["termination"]
+    assert res["breakdown_kind"] == case["breakdown_kind"]
+    assert same(np.asarray(res["history"], dtype=np.float64), store[f"{name}/history"])
+    assert same(res["x"], store[f"{name}/x"])
+    assert res["true_final_residual"] == store[f"{name}/true_final_residual"][0]
+
+
 def test_generators_match_reference_formulas():
     a, b = orc.poisson2d(1)
     assert a.n_rows == 225 and a.nnz == 1065  # test_io.py:180-189 KAT
