@@ -189,6 +189,23 @@ def kernel_roofline(pk, dm, ctx, torch, b, iters=200):
             "kernels": rows}
 
 
+def classical_same_box(pk, method, a, b, ctx, pipelined_us, iters=40):
+    """The reference's classical driver (one kernel per BLAS op, a host read
+    per inner product; solvers.py:310-389 / 485-580) on the same B200 and the
+    same kernels library -- the paper's baseline, beside the pipelined number."""
+    cfg = pk.SolverConfig(fixed_iterations=iters, max_iterations=iters)
+    fn = pk.SOLVERS[(method, "classical")]
+    fn(a, b, config=pk.SolverConfig(fixed_iterations=3, max_iterations=3), context=ctx)
+    res = fn(a, b, config=cfg, context=ctx)
+    us = res.loop_seconds / res.iterations * 1e6
+    st = res.trace.steady_state()
+    return {"value": round(us, 3), "unit": "us/iter", "iterations": res.iterations,
+            "launches_per_iteration": st.launches, "host_reads_per_iteration": st.transfers,
+            "pipelined_speedup": round(us / pipelined_us, 2),
+            "note": f"{method}_classical on this GPU, {iters} fixed iterations, loop wall time "
+                    "(host-driven: each inner product is a device->host read)"}
+
+
 def run_workload(args, world, rank, local):
     """Non-default workloads (BASELINE configs[0], [2], [3], [4]); same JSON
     contract, `config.workload` names the config.  Not the driver's headline
@@ -262,6 +279,7 @@ def run_workload(args, world, rank, local):
                                 "iterations": res.iterations, "reduction_geometry": "128x256",
                                 "l2": "working set 31 MB < 126 MB L2: latency/L2-bound"},
                      "time_to_tolerance_s": round(wall, 5),
+                     "classical_gpu": classical_same_box(pk, "cg", a, b, ctx, us),
                      "iteration_roofline": {"bytes_per_iteration": byt,
                                             "achieved_gbs": round(byt / (us * 1e-6) / 1e9, 1)},
                      "termination": res.termination})
@@ -418,6 +436,7 @@ def main():
         "gpu_launches": int(res.diagnostics.get("launches_per_iteration", 3)) * args.steps,
         "clocks": clk.summary(),
         "termination": res.termination,
+        "classical_gpu": classical_same_box(pk, "bicgstab", a_host, b_host, ctx, us_iter),
     }
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_reference(
