@@ -357,3 +357,20 @@ def test_c4_partitioned_random_rhs_fixed_iterations(pk):
     assert_identical(res, oracle_run("cg", a, b, (geom.n_groups, geom.group_size), fixed=25, max_iterations=25))
     single = pk.cg_pipelined(a, b, config=cfg, context=geom)
     assert same(single.x, res.x) and same(single.residual_history, res.residual_history)
+
+
+@pytest.mark.parametrize("n,k", [(3000, 5), (2000, 40), (600, 400)])
+def test_matrix_market_unstructured_rows(pk, tmp_path, n, k):
+    """Unstructured rows: the reference's random family
+    written to / read from Matrix Market, rows of 5, 40 (several SpMV passes)
+    and 400 entries; pipelined and classical drivers bitwise vs the oracle."""
+    a0, b = pk.gen_random_rowwise(n, k, seed=k)
+    path = tmp_path / "rand.mtx"
+    pk.write_matrix_market(path, a0)
+    a = pk.read_matrix_market(path)
+    assert a.equals(a0)
+    for method in ("bicgstab", "gmres"):
+        res = pk.SOLVERS[(method, "pipelined")](a, b, config=pk.SolverConfig(max_iterations=60))
+        assert_identical(res, oracle_run(method, a, b, (128, 256), max_iterations=60))
+        res = pk.SOLVERS[(method, "classical")](a, b, config=pk.SolverConfig(max_iterations=60))
+        assert_identical(res, orc.CLASSICAL[method](a, b, geom=(128, 256), max_iterations=60))

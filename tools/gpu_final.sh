@@ -2,8 +2,9 @@
 # Round-end measurement pass (one gpurun call): smoke, GPU tests, headline
 # bench + reference arm, launch list, ncu of the loop kernels, other configs.
 set -u
-OUT=gpurun_out/final; mkdir -p $OUT
-bash tools/gpu_round.sh final smoke tests bench launches ncu ncu_cg
+TAG=${1:-final}
+OUT=gpurun_out/$TAG; mkdir -p $OUT
+bash tools/gpu_round.sh $TAG smoke tests bench launches ncu ncu_cg
 timeout 900 python bench.py --workload c1 --steps 30 > $OUT/c1.json 2> $OUT/c1.err; echo "c1 rc=$?"
 timeout 900 python bench.py --workload c4 --steps 30 --warmup 3 > $OUT/c4_512.json 2> $OUT/c4.err; echo "c4 rc=$?"
 timeout 900 python bench.py --workload c4 --side 256 --steps 30 --warmup 3 > $OUT/c4_256.json 2>> $OUT/c4.err; echo "c4b rc=$?"
