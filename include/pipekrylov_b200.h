@@ -77,6 +77,7 @@ extern "C" {
 typedef struct pk_ctx pk_ctx; /* device + stream + reduction geometry */
 typedef struct pk_mat pk_mat; /* device-resident CSR matrix           */
 typedef struct pk_dcg pk_dcg; /* row-partitioned CG solver (C4)       */
+typedef struct pk_ell pk_ell; /* device-resident ELLPACK matrix       */
 
 /* SolverConfig (solvers.py:104-145).  fixed_iterations <= 0 means None. */
 typedef struct pk_config {
@@ -180,6 +181,18 @@ int pk_reduce_stage1(pk_ctx* ctx, int64_t n, int32_t nq, const double* const* co
 int pk_reduce_stage2(pk_ctx* ctx, int32_t nq, const double* partials, double* totals);
 /* dot (linalg.py:351-365): total written to device *total. */
 int pk_dot(pk_ctx* ctx, int64_t n, const double* x, const double* y, double* total);
+/* ELLPACK (linalg.py:179-246): width slots per row, column-major (slot k
+ * of row i at i + k n_rows), padded slots carry the sentinel column n_cols
+ * and value 0.  pk_ell_upload validates like EllMatrix.__post_init__
+ * (linalg.py:193-208) and stores int32 columns + fp64 values in HBM. */
+int pk_ell_upload(pk_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t width, const int64_t* col_indices,
+                  const double* values, pk_ell** out);
+int pk_ell_destroy(pk_ell* ell);
+/* spmv_ell (linalg.py:383-390, _spmvkernels.py:21-34): thread per row,
+ * coalesced slot loads, padded slots skipped -> bit-identical to pk_spmv on
+ * the same matrix in CSR form. */
+int pk_spmv_ell(pk_ctx* ctx, const pk_ell* a, const double* p, double* q);
+
 /* Classical-driver vector updates, one launch each (linalg.py:403-457,
  * solvers.py:277-280, 477-482), IEEE mul/add with no contraction, in the
  * NumPy expression order of the reference:

@@ -94,6 +94,21 @@ def csr_spmv(a, x):
     return acc
 
 
+def ell_spmv(n_rows, n_cols, width, cols, vals, x):
+    """ELLPACK product (_spmvkernels.py:21-34): slot k of row i at
+    i + k n_rows, sentinel column n_cols skipped (not multiplied by 0), slots
+    in order -- vectorised over rows, sequential over slots."""
+    x = np.asarray(x, dtype=np.float64)
+    acc = np.zeros(n_rows)
+    rows = np.arange(n_rows)
+    for k in range(width):
+        c = np.asarray(cols[k * n_rows:(k + 1) * n_rows])
+        live = c < n_cols
+        r = rows[live]
+        acc[r] = acc[r] + np.asarray(vals[k * n_rows:(k + 1) * n_rows])[live] * x[c[live]]
+    return acc
+
+
 def stage1(contrib, n_groups=DEFAULT_N_GROUPS, group_size=DEFAULT_GROUP_SIZE):
     """Grid-stride lanes + per-group halving tree (linalg.py:289-308).
 

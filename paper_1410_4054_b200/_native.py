@@ -94,6 +94,9 @@ SIGNATURES = {
     "pk_reduce_stage1": [_P, C.c_int64, C.c_int32, C.POINTER(_P), _P],
     "pk_reduce_stage2": [_P, C.c_int32, _P, _P],
     "pk_dot": [_P, C.c_int64, _P, _P, _P],
+    "pk_ell_upload": [_P, C.c_int64, C.c_int64, C.c_int64, _P, _P, _P],
+    "pk_ell_destroy": [_P],
+    "pk_spmv_ell": [_P, _P, _P, _P],
     "pk_vec_update": [_P, C.c_int32, C.c_int64, _P, _P, _P, C.c_double, C.c_double],
     "pk_cg_update": [_P, C.c_int64, _P, _P, _P, _P, C.c_double, C.c_double, _P],
     "pk_bicg_s_update": [_P, C.c_int64, _P, _P, _P, _P, C.c_double, _P, _P, _P, _P],

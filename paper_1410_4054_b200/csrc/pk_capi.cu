@@ -110,6 +110,13 @@ struct pk_mat {
   double* vals = nullptr;
 };
 
+struct pk_ell {
+  int device = 0;
+  int64_t n_rows = 0, n_cols = 0, width = 0;
+  int32_t* cols = nullptr;  // [width][n_rows], sentinel n_cols on padded slots
+  double* vals = nullptr;
+};
+
 static int set_device(int dev) {
   PK_CUDA(cudaSetDevice(dev));
   return PK_OK;
@@ -1137,6 +1144,95 @@ extern "C" int pk_spmv(pk_ctx* c, const pk_mat* a, const double* p, double* q) {
   if (!a || (!p && a->n_cols) || (!q && a->n_rows)) return fail(PK_ERR_INVALID, "NULL argument");
   if (a->n_rows == 0) return PK_OK;
   return spmv_fused_any(c, c->stream, a, p, q, 0, nullptr, nullptr, nullptr, 0, 0);
+}
+
+// ELLPACK SpMV (_spmvkernels.py:21-34): thread per row; slot k of the 32
+// rows of a warp is 32 consecutive words (coalesced, no L1 reuse needed);
+// EU slots' loads issued before their ordered adds; padded slots skipped.
+__global__ void __launch_bounds__(256) k_spmv_ell(int64_t n, int64_t n_cols, int64_t width,
+                                                  const int32_t* __restrict__ cols,
+                                                  const double* __restrict__ vals, const double* __restrict__ p,
+                                                  double* __restrict__ q) {
+  constexpr int EU = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double acc = 0.0;
+    int64_t k = 0;
+    for (; k + EU <= width; k += EU) {
+      int32_t c[EU];
+      double v[EU], x[EU];
+#pragma unroll
+      for (int u = 0; u < EU; ++u) {
+        c[u] = __ldg(cols + (k + u) * n + i);
+        v[u] = __ldg(vals + (k + u) * n + i);
+      }
+#pragma unroll
+      for (int u = 0; u < EU; ++u) x[u] = c[u] < n_cols ? __ldg(p + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < EU; ++u)
+        if (c[u] < n_cols) acc = add_rn(acc, mul_rn(v[u], x[u]));
+    }
+    for (; k < width; ++k) {
+      const int32_t c = __ldg(cols + k * n + i);
+      if (c < n_cols) acc = add_rn(acc, mul_rn(__ldg(vals + k * n + i), __ldg(p + c)));
+    }
+    q[i] = acc;
+  }
+}
+
+extern "C" int pk_ell_upload(pk_ctx* c, int64_t n_rows, int64_t n_cols, int64_t width, const int64_t* cols,
+                             const double* vals, pk_ell** out) {
+  if (!c || !out) return fail(PK_ERR_INVALID, "NULL argument");
+  *out = nullptr;
+  if (n_rows < 0 || n_cols < 0 || width < 0) return fail(PK_ERR_INVALID, "matrix dimensions must be non-negative");
+  if (n_rows >= (1ll << 31) - 1 || n_cols >= (1ll << 31) - 1)
+    return fail(PK_ERR_UNSUPPORTED, "device path indexes rows and columns with int32");
+  const int64_t total = n_rows * width;
+  if (total && (!cols || !vals)) return fail(PK_ERR_INVALID, "NULL argument");
+  std::vector<int32_t> c32((size_t)total);
+  for (int64_t t = 0; t < total; ++t) {
+    if (cols[t] < 0 || cols[t] > n_cols) return fail(PK_ERR_INVALID, "column index out of range");
+    if (cols[t] == n_cols && vals[t] != 0.0) return fail(PK_ERR_INVALID, "padded slots must store value 0");
+    c32[(size_t)t] = (int32_t)cols[t];
+  }
+  PK_TRY(set_device(c->device));
+  pk_ell* e = new pk_ell();
+  e->device = c->device;
+  e->n_rows = n_rows;
+  e->n_cols = n_cols;
+  e->width = width;
+  cudaError_t err = cudaSuccess;
+  if (total) {
+    err = cudaMalloc(&e->cols, (size_t)total * sizeof(int32_t));
+    if (err == cudaSuccess) err = cudaMalloc(&e->vals, (size_t)total * sizeof(double));
+    if (err == cudaSuccess) err = cudaMemcpy(e->cols, c32.data(), (size_t)total * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(e->vals, vals, (size_t)total * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  if (err != cudaSuccess) {
+    pk_ell_destroy(e);
+    return fail(PK_ERR_CUDA, std::string("ELL upload: ") + cudaGetErrorString(err));
+  }
+  *out = e;
+  return PK_OK;
+}
+
+extern "C" int pk_ell_destroy(pk_ell* e) {
+  if (!e) return PK_OK;
+  cudaSetDevice(e->device);
+  if (e->cols) cudaFree(e->cols);
+  if (e->vals) cudaFree(e->vals);
+  delete e;
+  return PK_OK;
+}
+
+extern "C" int pk_spmv_ell(pk_ctx* c, const pk_ell* a, const double* p, double* q) {
+  PK_CHECK_CTX(c);
+  if (!a || (!p && a->n_cols) || (!q && a->n_rows)) return fail(PK_ERR_INVALID, "NULL argument");
+  if (a->n_rows == 0) return PK_OK;
+  k_spmv_ell<<<grid_elem(c, a->n_rows, 256), 256, 0, c->stream>>>(a->n_rows, a->n_cols, a->width, a->cols, a->vals,
+                                                                  p, q);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
 }
 
 extern "C" int pk_spmv_fused(pk_ctx* c, const pk_mat* a, const double* p, double* q, int32_t nq,

@@ -28,6 +28,13 @@
 #include "pk_reduce.cuh"
 #include "pk_state.cuh"
 
+#ifndef PK_S2_SU
+#define PK_S2_SU 0  // stage-2 staging: 0 = one load per loop trip; N = N loads per lane in flight
+#endif
+#ifndef PK_FIN_PREFETCH
+#define PK_FIN_PREFETCH 0
+#endif
+
 #ifndef PK_BICGB_MINB
 #define PK_BICGB_MINB 4
 #endif
@@ -132,10 +139,33 @@ __device__ __noinline__ void stage2_warp(const S2Col* cols, int ng, double* out,
   for (int g0 = 0; g0 < ng; g0 += CH) {
     const int cnt = (ng - g0) < CH ? (ng - g0) : CH;
     __syncwarp();
+#if PK_S2_SU > 0
+    // PK_S2_SU loads per lane in flight before the shared-memory stores
+    for (int base = 0; base < cnt * NC; base += 32 * PK_S2_SU) {
+      double v[PK_S2_SU];
+#pragma unroll
+      for (int u = 0; u < PK_S2_SU; ++u) {
+        const int idx = base + u * 32 + lane;
+        if (idx < cnt * NC) {
+          const int c = idx / cnt, g = idx - c * cnt;
+          v[u] = __ldcg(cols[c].part + (int64_t)(g0 + g) * cols[c].ld + cols[c].col);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < PK_S2_SU; ++u) {
+        const int idx = base + u * 32 + lane;
+        if (idx < cnt * NC) {
+          const int c = idx / cnt, g = idx - c * cnt;
+          buf[c * CH + g] = v[u];
+        }
+      }
+    }
+#else
     for (int idx = lane; idx < cnt * NC; idx += 32) {
       const int c = idx / cnt, g = idx - c * cnt;
       buf[c * CH + g] = __ldcg(cols[c].part + (int64_t)(g0 + g) * cols[c].ld + cols[c].col);
     }
+#endif
     __syncwarp();
     if (lane < NC) {
       const double* b = buf + lane * CH;
@@ -159,6 +189,9 @@ __device__ __noinline__ void stage2_warp(const S2Col* cols, int ng, double* out,
 // the launching kernel's dynamic shared memory, free by the time it finalizes)
 __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing, double* buf, int buf_d) {
   const int th = threadIdx.x & 31;  // executed by one warp
+#if PK_FIN_PREFETCH
+  if (th < (int)((sizeof(SolveState) + 127) / 128)) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)st + th * 128));
+#endif
   const int ng = st->n_groups;
   double tot[4];
   switch (fin) {
