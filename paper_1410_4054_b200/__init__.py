@@ -49,6 +49,7 @@ from .solvers import (
 
 from .mmio import MatrixMarketError, gen_random_rowwise, gen_system, read_matrix_market, write_matrix_market  # noqa: E402
 from .ell import EllMatrix, csr_to_ell, ell_to_csr, spmv_ell  # noqa: E402
+from .execmodel import DeviceProfile, LatencyBarrier, calibrate_b200, latency_barrier, predict_iteration_time, speedup_curve  # noqa: E402,E501
 from .classical import bicgstab_classical, cg_classical, gmres_classical, orthogonalize_mgs  # noqa: E402
 
 # the reference's classical drivers (solvers.py:310-389, 485-580, 725-858) on
@@ -68,6 +69,7 @@ __all__ = [
     "SolverResult", "UpperTriangular", "WorkgroupPartials", "as_vector", "bicgstab_classical", "bicgstab_pipelined",
     "cg_classical", "gmres_classical", "orthogonalize_mgs", "MatrixMarketError", "gen_random_rowwise",
     "gen_system", "read_matrix_market", "write_matrix_market", "EllMatrix", "csr_to_ell", "ell_to_csr", "spmv_ell",
+    "DeviceProfile", "LatencyBarrier", "calibrate_b200", "latency_barrier", "predict_iteration_time", "speedup_curve",
     "cg_partitioned", "cg_pipelined", "context_for", "convdiff2d", "convdiff3d", "device_matrix", "gen_poisson2d",
     "gen_poisson3d_block", "gmres_pipelined", "poisson2d_grid", "poisson3d_grid", "solve", "solve_batch",
     "slab_geometry", "solve_upper_triangular", "__version__",
