@@ -422,6 +422,12 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
       const int F = 1 << geo.logf;
       const int cp = (int)(unit & (F - 1));
       const int msub = geo.m >> geo.logf;  // visits of this part: [cp msub, (cp + 1) msub)
+      if ((int64_t)g * geo.gs >= geo.n) {
+        // empty group (every lane past n): its tree of +0.0 lanes is +0.0
+        // (linalg.py:299-307 starts the lanes from zeros); part 0 publishes it
+        if (cp == 0 && part && tid < nstore) part[(int64_t)g * ld + col0 + tid] = 0.0;
+        ncomplete = cp == 0 ? 1 : 0;
+      } else {
       double out[QPW];
 #pragma unroll
       for (int i = 0; i < QPW; ++i) out[i] = 0.0;
@@ -501,6 +507,7 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         }
       }
       ncomplete = fin_group ? 1 : 0;
+      }
     }
     // ---- global ticket: the CTA completing the last group finalizes ----
     if (ncomplete > 0) {
