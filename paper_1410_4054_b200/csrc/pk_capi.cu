@@ -98,7 +98,8 @@ struct pk_ctx {
                                   // measured slower than the fused engine on C2, profiles/ENGINE_EXPERIMENTS.md)
   double* mat = nullptr;          // its contribution buffer, mat_cap doubles
   size_t mat_cap = 0;
-  bool mat_discard = true;        // PK_MAT_DISCARD=0: keep consumed lines in L2 (write-back on eviction)
+  bool mat_discard = true;
+  bool warp_k1 = true;            // PK_WARP_K1: n <= G systems on the warp chain engine (vs LEAF)        // PK_MAT_DISCARD=0: keep consumed lines in L2 (write-back on eviction)
 };
 
 struct pk_mat {
@@ -490,6 +491,15 @@ __global__ void k_row_max(const int64_t* counts, int64_t n, unsigned long long* 
 // quantities.  Must be called outside stream capture (it may reallocate).
 static int64_t min_units(const pk_ctx* c) { return (int64_t)c->sm_count * 4; }
 
+// single-chunk lanes on the warp engine instead of LEAF when at least a
+// quarter of the G <= 2^20 lanes hold a row (CG 128^2 at 128 x 256: 22 -> 16.8
+// us/iter, C5 108 -> 118 systems/s); sparser lane sets keep LEAF, whose
+// zero-fill unit skips the empty groups (n = 225: 12.5 vs 16.5 us/iter).
+// PK_WARP_K1=0 turns it off.
+static bool warp_k1(const pk_ctx* c, const Geom& geo) {
+  return c->warp_k1 && geo.G <= (int64_t)1 << 20 && 4 * geo.n >= geo.G;
+}
+
 static bool mat_applies(const pk_ctx* c, const Geom& geo) {
   return c->mat_mink > 0 && !geo.leaf && geo.K >= c->mat_mink;
 }
@@ -514,8 +524,10 @@ static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
       c->mat_cap = mneed;
     }
   }
-  if (geo.leaf && geo.logf == 0) return PK_OK;
-  size_t need = geo.leaf ? (size_t)geo.units * 32 * (size_t)std::max(nq, 1) : (size_t)geo.G * (size_t)std::max(nq, 1);
+  const bool k1 = geo.leaf && geo.K == 1 && warp_k1(c, geo);
+  if (geo.leaf && geo.logf == 0 && !k1) return PK_OK;
+  size_t need = geo.leaf && !k1 ? (size_t)geo.units * 32 * (size_t)std::max(nq, 1)
+                                : (size_t)geo.G * (size_t)std::max(nq, 1);
   if (need <= c->spill_cap) return PK_OK;
   PK_CUDA(cudaStreamSynchronize(c->stream));
   if (c->spill) cudaFree(c->spill);
@@ -595,7 +607,14 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
     }
   }
   if constexpr (NQ <= 4) {
-  if (!geo.leaf && geo.gs >= 32 && geo.K >= 2 && geo.K <= 8) {
+  // single-chunk lanes (n <= G) also go to the warp engine when the context
+  // allows it (PK_WARP_K1): one warp per 32 lanes, no leaf stacks or splits
+  const bool k1 = geo.leaf && geo.K == 1 && warp_k1(c, geo);
+  const Geom gw = k1 ? make_geom(n, c->ng, c->gs, min_units(c), true) : geo;
+  if (k1 && (size_t)gw.G * (size_t)nstore > c->spill_cap)
+    return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
+  if (!gw.leaf && gw.gs >= 32 && gw.K >= (k1 ? 1 : 2) && gw.K <= 8) {
+    const Geom& geo = gw;
     // warp-per-unit chain engine (no shared staging, no CTA barrier): wins
     // for short chains (small, latency-bound systems, e.g. CG 512^2: 20.6 vs
     // 26.8 us/iter); long chains keep the CTA engine (C2: 44.7 vs 63.8 us)
@@ -838,6 +857,7 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e2 = getenv("PK_PDL")) c->pdl = atoi(e2) != 0;
   if (const char* e3 = getenv("PK_MAT_MINK")) c->mat_mink = atoi(e3);
   if (const char* e4 = getenv("PK_MAT_DISCARD")) c->mat_discard = atoi(e4) != 0;
+  if (const char* e5 = getenv("PK_WARP_K1")) c->warp_k1 = atoi(e5) != 0;
   // keep freed workspace memory in the stream-ordered pool between solves
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {

@@ -64,7 +64,9 @@ struct Geom {
   int32_t leaf;    // 1 = LEAF mapping
   int32_t m;       // LEAF: leaves per lane thread (gs / 32)
   int32_t logm;
-  int32_t logf;    // LEAF: a group is split over F = 2^logf CTAs (units = n_groups F)
+  int32_t logf;    // LEAF: a group is split over F = 2^logf CTAs (units = ne F [+ 1])
+  int32_t ne;      // LEAF: groups holding at least one row (ceil(n / gs), <= n_groups); the
+                   // rest are all-zero and published by one extra zero-fill unit
   int32_t tT;      // CHAIN group tree: threads = min(gs, kThreads)
   int32_t tm;      // CHAIN group tree: leaves per tree thread
   int32_t tlogm;
@@ -73,7 +75,9 @@ struct Geom {
 // min_units: LEAF groups are split over F = 2^logf CTAs (each a contiguous
 // range of bit-reversed visits = a complete sub-tree) until n_groups F >=
 // min_units, so that few large groups still fill the GPU.
-inline Geom make_geom(int64_t n, int32_t n_groups, int32_t gs, int64_t min_units = 0) {
+// chain_only: CHAIN mapping even for K = 1 (the warp engine's single-chunk
+// lanes: lane value = 0.0 + c, exactly the reference's zeros + chunk).
+inline Geom make_geom(int64_t n, int32_t n_groups, int32_t gs, int64_t min_units = 0, bool chain_only = false) {
   Geom g{};
   g.n = n;
   g.n_groups = n_groups;
@@ -81,13 +85,15 @@ inline Geom make_geom(int64_t n, int32_t n_groups, int32_t gs, int64_t min_units
   g.G = (int64_t)n_groups * gs;
   int64_t k = (n + g.G - 1) / g.G;
   g.K = k < 1 ? 1 : k;
-  g.leaf = (g.K == 1 && gs >= 32) ? 1 : 0;
+  g.leaf = (g.K == 1 && gs >= 32 && !chain_only) ? 1 : 0;
   if (g.leaf) {
     g.m = gs / 32;
     g.logm = ilog2_u((uint32_t)g.m);
+    const int64_t ne = (n + gs - 1) / gs;
+    g.ne = (int32_t)(ne < n_groups ? ne : n_groups);
     g.logf = 0;
-    while ((int64_t)n_groups << g.logf < min_units && (1 << (g.logf + 1)) <= g.m) ++g.logf;
-    g.units = (int64_t)n_groups << g.logf;
+    while ((int64_t)g.ne << g.logf < min_units && (1 << (g.logf + 1)) <= g.m) ++g.logf;
+    g.units = ((int64_t)g.ne << g.logf) + (g.ne < n_groups ? 1 : 0);
   } else {
     g.units = (g.G + 31) / 32;
     g.tT = gs < kThreads ? gs : kThreads;
@@ -417,6 +423,14 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         ncomplete = g1 - g0;
       }
     } else {
+      if (unit >= ((int64_t)geo.ne << geo.logf)) {
+        // the zero-fill unit: groups [ne, n_groups) lie wholly past n; their
+        // tree of +0.0 lanes is +0.0 (linalg.py:299-307 starts from zeros)
+        if (part)
+          for (int64_t t = tid; t < (int64_t)(geo.n_groups - geo.ne) * nstore; t += kThreads)
+            part[(int64_t)(geo.ne + t / nstore) * ld + col0 + t % nstore] = 0.0;
+        ncomplete = geo.n_groups - geo.ne;
+      } else {
       // ---- LEAF: group g, part cp of F; the folding lane owns lanes {lane + 32 j} ----
       const int g = (int)(unit >> geo.logf);
       const int F = 1 << geo.logf;
@@ -507,6 +521,7 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         }
       }
       ncomplete = fin_group ? 1 : 0;
+      }
       }
     }
     // ---- global ticket: the CTA completing the last group finalizes ----
