@@ -283,6 +283,42 @@ def run_workload(args, world, rank, local):
                      "iteration_roofline": {"bytes_per_iteration": byt,
                                             "achieved_gbs": round(byt / (us * 1e-6) / 1e9, 1)},
                      "termination": res.termination})
+    elif args.workload == "c3":
+        from paper_1410_4054_b200.solvers import solve_resident
+
+        side, m = 128, 30
+        ctx = pk.ExecutionContext(128, 256, device=dev)
+        dm, b_host = pk.convdiff3d(side, device=True, context=ctx)
+        b = torch.from_numpy(b_host).to("cuda")
+        iters = max(args.steps // m, 1) * m  # whole restart cycles
+        solve_resident("gmres", dm, b, config=pk.SolverConfig(fixed_iterations=m, max_iterations=m), context=ctx)
+        cfg = pk.SolverConfig(fixed_iterations=iters, max_iterations=iters, restart=m)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, res = solve_resident("gmres", dm, b, config=cfg, context=ctx)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        n, nnz = dm.n_rows, dm.nnz
+        us_inner = res.loop_seconds / res.iterations * 1e6
+        us_full = wall / res.iterations * 1e6
+        # step i of a cycle: B_CSR + 40 n (i = 1), B_CSR + 56 n + 16 n (i - 1) (i >= 2); per cycle the
+        # x update adds 8 n (m + 2)
+        steps = sum(b_csr(n, nnz) + (40 * n if i == 1 else 56 * n + 16 * n * (i - 1)) for i in range(1, m + 1))
+        per_iter_inner = steps / m
+        per_iter_full = (steps + 8 * n * (m + 2)) / m
+        line.update({"value": round(us_inner, 3), "ms_per_step": round(us_inner / 1e3, 6), "scaling": "weak",
+                     "config": {"workload": f"pipelined GMRES({m}), 3D 7-point upwind convection-diffusion {side}^3 "
+                                            "(configs[2])", "n": n, "nnz": nnz, "iterations": res.iterations,
+                                "cycles": res.iterations // m, "reduction_geometry": "128x256",
+                                "value_is": "inner Arnoldi loop time / iteration (the reference's loop_seconds "
+                                            "protocol, solvers.py:928/953)"},
+                     "full_cycle_us_per_iter": round(us_full, 3),
+                     "iteration_roofline": {"bytes_per_iteration_inner": int(per_iter_inner),
+                                            "achieved_gbs_inner": round(per_iter_inner / (us_inner * 1e-6) / 1e9, 1),
+                                            "frac_inner": round(per_iter_inner / (us_inner * 1e-6) / 1e9 / peak, 4),
+                                            "bytes_per_iteration_full": int(per_iter_full),
+                                            "frac_full": round(per_iter_full / (us_full * 1e-6) / 1e9 / peak, 4)},
+                     "termination": res.termination})
     elif args.workload == "c5":
         nsys_total = args.nsys
         sides = [128, 256, 512]
@@ -328,7 +364,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--loop", default="graph", choices=["graph", "host"],
                     help="iteration loop driver (host: per-launch kernels visible to ncu)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c4", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c1", "c3", "c4", "c5"],
                     help="c2 = configs[1] (default, the headline); c1/c4/c5 = configs[0]/[3]/[4]")
     ap.add_argument("--side", type=int, default=None, help="c4 grid side (default 512)")
     ap.add_argument("--nsys", type=int, default=4096, help="c5 number of systems")

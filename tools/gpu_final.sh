@@ -6,6 +6,7 @@ TAG=${1:-final}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 bash tools/gpu_round.sh $TAG smoke tests bench launches ncu ncu_cg
 timeout 900 python bench.py --workload c1 --steps 30 > $OUT/c1.json 2> $OUT/c1.err; echo "c1 rc=$?"
+timeout 900 python bench.py --workload c3 --steps 300 --warmup 3 > $OUT/c3.json 2> $OUT/c3.err; echo "c3 rc=$?"
 timeout 900 python bench.py --workload c4 --steps 30 --warmup 3 > $OUT/c4_512.json 2> $OUT/c4.err; echo "c4 rc=$?"
 timeout 900 python bench.py --workload c4 --side 256 --steps 30 --warmup 3 > $OUT/c4_256.json 2>> $OUT/c4.err; echo "c4b rc=$?"
 timeout 900 python bench.py --workload c5 --nsys 192 > $OUT/c5_192.json 2> $OUT/c5.err; echo "c5 rc=$?"
