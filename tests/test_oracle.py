@@ -178,3 +178,23 @@ def test_solvers_match_live_reference(ref, method, geom):
     assert same(np.asarray(oo["history"]), np.asarray(rr.residual_history))
     assert same(oo["x"], rr.x)
     assert oo["true_final_residual"] == rr.true_final_residual
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("method", ["cg", "bicgstab", "gmres"])
+@pytest.mark.parametrize("geom", [(128, 256), (7, 64)])
+def test_classical_match_live_reference(ref, method, geom):
+    """Oracle classical drivers vs the live reference's classical drivers on a
+    fresh random-RHS case (GMRES with CGS and MGS)."""
+    a, _ = ref.gen_poisson2d(3)
+    rhs = np.random.default_rng(8).random(a.n_rows)
+    ctx = ref.ExecutionContext(n_groups=geom[0], group_size=geom[1])
+    for mgs in ((False, True) if method == "gmres" else (False,)):
+        kw = {"orthogonalization": "modified_gs"} if mgs else {}
+        rr = ref.SOLVERS[(method, "classical")](a, rhs, config=ref.SolverConfig(max_iterations=120, **kw), context=ctx)
+        okw = {"mgs": mgs} if method == "gmres" else {}
+        oo = orc.CLASSICAL[method](a, rhs, max_iterations=120, geom=geom, **okw)
+        assert oo["iterations"] == rr.iterations and oo["termination"] == rr.termination
+        assert same(np.asarray(oo["history"]), np.asarray(rr.residual_history))
+        assert same(oo["x"], rr.x)
+        assert oo["true_final_residual"] == rr.true_final_residual
