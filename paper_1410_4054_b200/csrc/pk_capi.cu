@@ -99,6 +99,7 @@ struct pk_ctx {
   double* mat = nullptr;          // its contribution buffer, mat_cap doubles
   size_t mat_cap = 0;
   bool mat_discard = true;
+  bool sweep_one_batch = false;   // PK_SWEEP_ONEBATCH: elementwise sweeps with one V-row batch per thread
   bool warp_k1 = true;            // PK_WARP_K1: n <= G systems on the warp chain engine (vs LEAF)        // PK_MAT_DISCARD=0: keep consumed lines in L2 (write-back on eviction)
 };
 
@@ -647,8 +648,12 @@ template <class Op>
 static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp = ScalarPtrs{},
                         SolveState* st = nullptr, int gate = GATE_NONE) {
   auto kern = k_sweep<Op>;
-  PK_CUDA(launch_k(c->pdl, kern, dim3(engine_grid(c, kern, 0, (n + 255) / 256, 256)), dim3(256), 0, s, n, op, sp, st,
-                   gate));
+  // sweep_one_batch: one CTA per 256 x PK_SWEEP_V rows (several waves), so
+  // every thread's rows are a single batch of loads in flight; otherwise the
+  // grid is capped at the resident CTAs and threads loop
+  int64_t grid = engine_grid(c, kern, 0, (n + 255) / 256, 256);
+  if (c->sweep_one_batch && !Op::kSpmv) grid = std::max<int64_t>(1, (n + 256 * PK_SWEEP_V - 1) / (256 * PK_SWEEP_V));
+  PK_CUDA(launch_k(c->pdl, kern, dim3((unsigned)grid), dim3(256), 0, s, n, op, sp, st, gate));
   return PK_OK;
 }
 
@@ -858,6 +863,7 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e3 = getenv("PK_MAT_MINK")) c->mat_mink = atoi(e3);
   if (const char* e4 = getenv("PK_MAT_DISCARD")) c->mat_discard = atoi(e4) != 0;
   if (const char* e5 = getenv("PK_WARP_K1")) c->warp_k1 = atoi(e5) != 0;
+  if (const char* e6 = getenv("PK_SWEEP_ONEBATCH")) c->sweep_one_batch = atoi(e6) != 0;
   // keep freed workspace memory in the stream-ordered pool between solves
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
