@@ -183,3 +183,45 @@ def test_long_rows_take_the_remainder_path(pk, fused):
         q, part = fused.spmv_fused(a, dev(p), ("input", "result"), pk.ExecutionContext(*geom))
         oq, opart = orc.spmv_fused(a, p, ("input", "result"), geom)
         assert same(host(q), oq) and same(host(part), opart)
+
+
+@pytest.mark.gpu
+def test_vec_update_kinds_bitwise():
+    """pk_vec_update: every kind equals the reference's NumPy expression
+    (linalg.py:403-457, solvers.py:277-280, 477-482) bit for bit, including
+    signed zeros, subnormals and non-finite inputs."""
+    import ctypes as C
+
+    import torch
+
+    import paper_1410_4054_b200 as pk
+    from paper_1410_4054_b200 import _native as N
+    from paper_1410_4054_b200.device import context_for
+
+    rng = np.random.default_rng(12)
+    n = 100_003
+    y0, x, z = (rng.standard_normal(n) * 10.0 ** rng.integers(-300, 300, n) for _ in range(3))
+    for v in (y0, x, z):
+        v[:8] = [0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 1.0]
+    a, bta = -0.3712, 1.9e3
+    want = {
+        N.VEC_AXPY: y0 + a * x,
+        N.VEC_AXPY2: y0 + (a * x + bta * z),
+        N.VEC_XPAY: y0 * bta + x,
+        N.VEC_SCALE: y0 * a,
+        N.VEC_ADD_SCALED: x + a * z,
+        N.VEC_BICG_P: (y0 - bta * z) * a + x,
+        N.VEC_COPY: x.copy(),
+    }
+    ctx = pk.ExecutionContext()
+    dc = context_for(ctx)
+    dc.set_stream(torch.cuda.current_stream())
+    xd, zd = torch.from_numpy(x).cuda(), torch.from_numpy(z).cuda()
+    with np.errstate(all="ignore"):
+        for kind, ref in want.items():
+            yd = torch.from_numpy(y0.copy()).cuda()
+            N.check(N.lib().pk_vec_update(dc.handle, kind, n, C.c_void_p(yd.data_ptr()), C.c_void_p(xd.data_ptr()),
+                                          C.c_void_p(zd.data_ptr()), a, bta), "vec")
+            got = yd.cpu().numpy()
+            assert np.array_equal(got.view(np.int64)[~np.isnan(ref)], ref.view(np.int64)[~np.isnan(ref)]), kind
+            assert np.array_equal(np.isnan(got), np.isnan(ref)), kind
