@@ -1,0 +1,41 @@
+#!/bin/bash
+# Commit-able SASS of the hot loop kernels (sm_100a) + an instruction-mix
+# summary: usage tools/dump_sass.sh [outdir]
+set -u
+OUT=${1:-profiles/sass}; mkdir -p "$OUT"
+LIB=paper_1410_4054_b200/libpk_b200.so
+cuobjdump -sass "$LIB" > /tmp/pk_all.sass
+python3 - "$OUT" <<'PY'
+import re, subprocess, sys
+out = sys.argv[1]
+text = open("/tmp/pk_all.sass").read()
+funcs = re.split(r"\n\s*Function : ", text)
+want = {"OpBicgB<int, 5>": "k_reduce_OpBicgB", "OpBicgApNext<int, 5>": "k_reduce_OpBicgApNext",
+        "k_sweep<pk::OpBicgXrpSweep>": "k_sweep_OpBicgXrpSweep", "OpCgFused<int, 5>": "k_reduce_warp_OpCgFused",
+        "k_spmv_ell": "k_spmv_ell", "k_vec_update<1>": "k_vec_update_axpy2"}
+rows = []
+for f in funcs[1:]:
+    name = f.split("\n", 1)[0].strip()
+    dem = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip()
+    for key, tag in want.items():
+        if key in dem and (("k_reduce<" in dem and "warp" not in tag) or ("k_reduce_warp<" in dem and "warp" in tag)
+                           or ("k_reduce" not in dem)):
+            if "k_reduce" in tag and "<4, 2, 4," not in dem and "<2, 2, 4," not in dem and "warp" not in tag:
+                continue
+            open(f"{out}/{tag}.sass", "w").write(dem + "\n" + f)
+            ins = re.findall(r"/\*[0-9a-f]{4,}\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]+)", f)
+            ops = [m[1] for m in ins]
+            cnt = lambda p: sum(1 for o in ops if o.startswith(p))
+            rows.append((tag, len(ops), cnt("LDG"), cnt("STG"), cnt("LDS"), cnt("DADD"), cnt("DMUL"), cnt("DFMA"),
+                         cnt("BAR"), cnt("ATOM") + cnt("RED")))
+            want.pop(key)
+            break
+with open(f"{out}/README.md", "w") as fh:
+    fh.write("# SASS of the hot kernels (sm_100a, cuobjdump -sass of libpk_b200.so)\n\n"
+             "Static instruction counts. DFMA appears only inside the correctly rounded div.rn / sqrt.rn\n"
+             "expansions of the finalizers (the row arithmetic is DMUL + DADD, -fmad=false).\n\n"
+             "| kernel | instructions | LDG | STG | LDS | DADD | DMUL | DFMA | BAR | ATOM/RED |\n|---|---|---|---|---|---|---|---|---|---|\n")
+    for r in rows:
+        fh.write("| " + " | ".join(str(v) for v in r) + " |\n")
+print(open(f"{out}/README.md").read())
+PY
