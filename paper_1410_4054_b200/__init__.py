@@ -32,6 +32,7 @@ from .solvers import (
     CONVERGED,
     DEFAULT_BREAKDOWN_TOLERANCE,
     LUCKY_BREAKDOWN,
+    LuckyBreakdown,
     MAX_ITER,
     MODIFIED_GS,
     SOLVERS,
@@ -50,6 +51,20 @@ from .solvers import (
 from .mmio import MatrixMarketError, gen_random_rowwise, gen_system, read_matrix_market, write_matrix_market  # noqa: E402
 from .ell import EllMatrix, csr_to_ell, ell_to_csr, spmv_ell  # noqa: E402
 from .execmodel import DeviceProfile, LatencyBarrier, calibrate_b200, latency_barrier, predict_iteration_time, speedup_curve  # noqa: E402,E501
+from .fused import (  # noqa: E402  kernel-level ops on CUDA tensors (fused.py / linalg.py mirrors)
+    FusedReductionRequest,
+    dot,
+    fused_bicgstab_s_update,
+    fused_bicgstab_xrp_update,
+    fused_cg_vector_update,
+    fused_gs_normalize,
+    fused_gs_stage1,
+    fused_gs_update,
+    reduce_stage1,
+    reduce_stage2,
+    spmv_csr,
+    spmv_fused,
+)
 from .classical import bicgstab_classical, cg_classical, gmres_classical, orthogonalize_mgs  # noqa: E402
 
 # the reference's classical drivers (solvers.py:310-389, 485-580, 725-858) on
@@ -72,5 +87,7 @@ __all__ = [
     "DeviceProfile", "LatencyBarrier", "calibrate_b200", "latency_barrier", "predict_iteration_time", "speedup_curve",
     "cg_partitioned", "cg_pipelined", "context_for", "convdiff2d", "convdiff3d", "device_matrix", "gen_poisson2d",
     "gen_poisson3d_block", "gmres_pipelined", "poisson2d_grid", "poisson3d_grid", "solve", "solve_batch",
-    "slab_geometry", "solve_upper_triangular", "__version__",
+    "slab_geometry", "solve_upper_triangular", "__version__", "LuckyBreakdown", "FusedReductionRequest", "dot",
+    "fused_bicgstab_s_update", "fused_bicgstab_xrp_update", "fused_cg_vector_update", "fused_gs_normalize",
+    "fused_gs_stage1", "fused_gs_update", "reduce_stage1", "reduce_stage2", "spmv_csr", "spmv_fused",
 ]

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     const int g = (int)(lid0 / geo.gs);
     if (tid == 0) {
       const unsigned per = (unsigned)(geo.gs / LPB);
-      unsigned tk = atomic_add_release(scr.gtick + g, 1u);
+      unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
       int last = (tk == per - 1);
       if (last) scr.gtick[g] = 0u;
       s_flag = last;
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 4)
     __syncthreads();
     if (tid == 0) {
       unsigned* ticket = st ? &st->ticket : scr.ticket;
-      unsigned tk = atomic_add_release(ticket, (unsigned)ncomplete);
+      unsigned tk = atomic_add_acq_rel(ticket, (unsigned)ncomplete);
       if (tk + (unsigned)ncomplete == (unsigned)geo.n_groups) {
         *ticket = 0u;
         s_last = 1;
@@ -543,10 +544,18 @@ static Scratch scratch_of(const pk_ctx* c) { return Scratch{c->spill, c->gtick, 
 
 // Raise a kernel's dynamic shared-memory limit when a launch needs more than
 // the default 48 KB minus its static shared memory (the finalizer's 8 KB
-// stage-2 staging buffer lives there); once per instantiation and size.
+// stage-2 staging buffer lives there).  The attribute is per device, so the
+// granted size is tracked per (device, kernel), under a lock (pk_solve_batch
+// workers launch concurrently), and is only ever raised.
+static std::mutex g_smem_mu;
+static std::map<std::pair<int, const void*>, size_t> g_smem_granted;
+
 template <class K>
 static int allow_dynamic_smem(K kern, size_t dyn) {
-  static size_t granted = 0;  // per template instantiation
+  int dev = 0;
+  PK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_smem_mu);
+  size_t& granted = g_smem_granted[{dev, (const void*)kern}];
   if (dyn <= granted) return PK_OK;
   cudaFuncAttributes fa;
   PK_CUDA(cudaFuncGetAttributes(&fa, kern));

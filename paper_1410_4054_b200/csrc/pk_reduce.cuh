@@ -293,13 +293,16 @@ __device__ __forceinline__ void group_tree(const Geom& geo, int g, const double*
 // the engine
 // ---------------------------------------------------------------------------
 
-// Ticket increment with release semantics at gpu scope: MEMBAR.ALL.GPU +
-// ATOM, without the L1 invalidation (CCTL.IVALL) that __threadfence() adds --
-// an invalidation would throw away the L1-resident CSR lines of every warp on
-// the SM.  Readers of the published data use L2 loads (ld.global.cg).
-__device__ __forceinline__ unsigned atomic_add_release(unsigned* p, unsigned v) {
+// Ticket increment with acquire-release semantics at gpu scope: the release
+// half publishes this CTA's spill/partials before the ticket moves, the
+// acquire half makes every other CTA's published data visible to the CTA
+// that draws the last ticket (it then reads them with L2 loads,
+// ld.global.cg).  No __threadfence(): that would also emit an L1
+// invalidation (CCTL.IVALL) and throw away the L1-resident CSR lines of every
+// warp on the SM.
+__device__ __forceinline__ unsigned atomic_add_acq_rel(unsigned* p, unsigned v) {
   unsigned r;
-  asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
   return r;
 }
 
@@ -405,7 +408,7 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         const int g = (int)(lid0 / geo.gs);
         if (tid == 0) {
           const unsigned per = (unsigned)(geo.gs / 32);
-          unsigned tk = atomic_add_release(scr.gtick + g, 1u);
+          unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
           int last = (tk == per - 1);
           if (last) scr.gtick[g] = 0u;
           s_flag = last;
@@ -484,7 +487,7 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         }
         __syncthreads();
         if (tid == 0) {
-          unsigned tk = atomic_add_release(scr.gtick + g, 1u);
+          unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
           int lastp = (tk == (unsigned)F - 1);
           if (lastp) scr.gtick[g] = 0u;
           s_flag = lastp;
@@ -528,7 +531,7 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
     if (ncomplete > 0) {
       __syncthreads();
       if (tid == 0) {
-        unsigned tk = atomic_add_release(ticket, (unsigned)ncomplete);
+        unsigned tk = atomic_add_acq_rel(ticket, (unsigned)ncomplete);
         if (tk + (unsigned)ncomplete == (unsigned)geo.n_groups) {
           *ticket = 0u;
           s_last = 1;
@@ -702,7 +705,7 @@ __device__ __forceinline__ bool engine_warp_chain(const Geom& geo, const Op& op,
     int lastg = 0;
     if (lane == 0) {
       const unsigned per = (unsigned)(geo.gs / 32);
-      unsigned tk = atomic_add_release(scr.gtick + g, 1u);
+      unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
       lastg = (tk == per - 1);
       if (lastg) scr.gtick[g] = 0u;
     }
@@ -711,7 +714,7 @@ __device__ __forceinline__ bool engine_warp_chain(const Geom& geo, const Op& op,
       group_tree_warp<NQ>(geo, g, scr.spill, stk, part, ld, col0, nstore);
       int l = 0;
       if (lane == 0) {
-        unsigned tk = atomic_add_release(ticket, 1u);
+        unsigned tk = atomic_add_acq_rel(ticket, 1u);
         if (tk + 1u == (unsigned)geo.n_groups) {
           *ticket = 0u;
           l = 1;

@@ -18,9 +18,33 @@ import torch
 from . import _native as N
 from .device import DeviceMatrix, context_for, device_matrix
 from .linalg import ExecutionContext
+from .solvers import BreakdownError, LuckyBreakdown
 
 WITH_INPUT = "input"
 WITH_RESULT = "result"
+
+
+class FusedReductionRequest:
+    """Inner products accumulated alongside a fused SpMV (fused.py:55-83):
+    each quantity is "input" (<q,p>), "result" (<q,q>) or a fixed vector w
+    (<q,w>, here a float64 CUDA tensor); 1 to 4 quantities per kernel."""
+
+    MAX_QUANTITIES = 4
+
+    def __init__(self, quantities):
+        quantities = tuple(quantities)
+        if not 1 <= len(quantities) <= self.MAX_QUANTITIES:
+            raise ValueError(f"request must carry 1 to {self.MAX_QUANTITIES} quantities, got {len(quantities)}")
+        for q in quantities:
+            if isinstance(q, str) and q not in (WITH_INPUT, WITH_RESULT):
+                raise ValueError(f"unknown quantity kind {q!r}")
+        self.quantities = quantities
+
+    def __len__(self) -> int:
+        return len(self.quantities)
+
+    def __iter__(self):
+        return iter(self.quantities)
 
 
 def _ptr(t):
@@ -48,7 +72,7 @@ def _partials(ctx, nq, device):
     return torch.empty((ctx.n_groups, nq), dtype=torch.float64, device=device)
 
 
-def spmv(a, p, ctx=None):
+def spmv_csr(a, p, ctx=None):
     """q = A p (spmv_csr, linalg.py:373-380)."""
     ctx, dc = _dc(ctx)
     dm = device_matrix(a, ctx)
@@ -66,9 +90,9 @@ def spmv_fused(a, p, quantities, ctx=None):
     ctx, dc = _dc(ctx)
     dm = device_matrix(a, ctx)
     p = _vec(p, dm.n_cols, "p")
-    quantities = tuple(quantities)
-    if not 1 <= len(quantities) <= 4:
-        raise ValueError(f"request must carry 1 to 4 quantities, got {len(quantities)}")
+    quantities = tuple(FusedReductionRequest(quantities))
+    if WITH_INPUT in [q for q in quantities if isinstance(q, str)] and dm.n_rows != dm.n_cols:
+        raise ValueError("result-with-input dot needs a square matrix")
     kinds = (C.c_int32 * 4)()
     ws = (C.c_void_p * 4)()
     keep = []
@@ -139,18 +163,6 @@ def fused_cg_vector_update(x, r, p, Ap, alpha, beta, ctx=None):
     return part
 
 
-class Breakdown(RuntimeError):
-    def __init__(self, kind):
-        super().__init__(f"breakdown: {kind}")
-        self.kind = kind
-
-
-class LuckyBreakdown(Exception):
-    def __init__(self, norm):
-        super().__init__(f"candidate basis vector has norm {norm!r}")
-        self.norm = norm
-
-
 def fused_bicgstab_s_update(r, Ap, rr0_partials, Apr0_partials, ctx=None, breakdown_tolerance=1e-30):
     """alpha finalized on the device; s = r - alpha Ap; <s,s> (fused.py:154-182)."""
     ctx, dc = _dc(ctx)
@@ -164,7 +176,7 @@ def fused_bicgstab_s_update(r, Ap, rr0_partials, Apr0_partials, ctx=None, breakd
                                      _ptr(Apr0_partials.contiguous()), float(breakdown_tolerance), _ptr(s),
                                      _ptr(part), _ptr(alpha), _ptr(flag)))
     if int(flag.item()):
-        raise Breakdown("Apr0star")
+        raise BreakdownError("Apr0star")
     return s, part, float(alpha.item())
 
 
@@ -224,3 +236,6 @@ def fused_gs_normalize(v, norm_partials, r, ctx=None, breakdown_tolerance=1e-30)
     if int(flag.item()):
         raise LuckyBreakdown(float(norm.item()))
     return float(norm.item()), part
+
+
+spmv = spmv_csr

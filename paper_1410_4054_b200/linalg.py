@@ -48,9 +48,12 @@ class CsrMatrix:
 
     def __init__(self, n_rows, n_cols, row_offsets, col_indices, values):
         n_rows, n_cols = int(n_rows), int(n_cols)
-        offs = np.ascontiguousarray(row_offsets, dtype=np.int64)
-        cols = np.ascontiguousarray(col_indices, dtype=np.int64)
-        vals = np.ascontiguousarray(values, dtype=np.float64)
+        # private copies: freezing them must not make the caller's arrays
+        # read-only, and later edits of the caller's buffers must not desync
+        # the cached HBM copy (the reference keeps its own arrays too)
+        offs = np.array(row_offsets, dtype=np.int64, copy=True)
+        cols = np.array(col_indices, dtype=np.int64, copy=True)
+        vals = np.array(values, dtype=np.float64, copy=True)
         if n_rows < 0 or n_cols < 0:
             raise ValueError("matrix dimensions must be non-negative")
         if offs.ndim != 1 or offs.shape[0] != n_rows + 1:

@@ -134,6 +134,8 @@ class PartitionedCG:
         res = N.PkResult()
         dp = C.POINTER(C.c_double)
         bb = None if b_local is None else np.ascontiguousarray(b_local, dtype=np.float64)
+        if bb is not None and bb.shape != (self.nloc,):
+            raise ValueError(f"b_local must have shape ({self.nloc},), got {bb.shape}")
         N.check(N.lib().pk_dcg_solve(self.h.h, bb.ctypes.data_as(dp) if bb is not None else None,
                                      C.byref(_native_config(cfg)), x.ctypes.data_as(dp), hist.ctypes.data_as(dp),
                                      len(hist), C.byref(res)), "pk_dcg_solve")

@@ -42,6 +42,14 @@ class BreakdownError(RuntimeError):
         super().__init__(message or f"breakdown: {kind}")
 
 
+class LuckyBreakdown(Exception):
+    """The GMRES candidate basis vector has (numerically) zero norm (errors.py:21-27)."""
+
+    def __init__(self, norm: float):
+        self.norm = norm
+        super().__init__(f"candidate basis vector has norm {norm!r}")
+
+
 @dataclass(frozen=True)
 class SolverConfig:
     """Driver knobs (solvers.py:104-145) plus ``loop_mode``: "graph" (CUDA
@@ -193,23 +201,53 @@ def _native_config(cfg: SolverConfig) -> N.PkConfig:
         loop_mode=N.LOOP_GRAPH if cfg.loop_mode == "graph" else N.LOOP_HOST, flags=0)
 
 
-def _trace_from(res: N.PkResult, method: str, n: int, restart: int) -> ExecutionTrace:
-    """ExecutionTrace filled with the launches/transfers really issued.
+def iteration_kernel_bytes(method: str, n: int, nnz: int, launches: int, step: int = 1) -> int:
+    """Algorithmic HBM bytes of one iteration's kernels as the library issues
+    them (int32 indices, fp64 values, every vector read/written once per
+    kernel, a gathered vector counted once): B_CSR = 12 nnz + 4 (n + 1).
+
+    CG: 1 kernel (OpCgFused) B_CSR + 64 n; 2 kernels (update sweep 56 n +
+    OpCgApNext B_CSR + 24 n).  BiCGStab: 2 kernels (OpBicgB B_CSR + 32 n +
+    OpBicgA B_CSR + 80 n); 3 kernels (OpBicgB + xrp sweep 64 n + OpBicgApNext
+    B_CSR + 32 n).  GMRES step i: SpMV B_CSR + 16 n, multi-dot 8 n (i - 1)
+    (i >= 3), GS update 8 n (i - 1) + 16 n (i >= 2), normalize 24 n."""
+    bcsr = 12 * nnz + 4 * (n + 1)
+    if method == "cg":
+        return bcsr + 64 * n if launches <= 1 else bcsr + 80 * n
+    if method == "bicgstab":
+        return 2 * bcsr + (112 * n if launches <= 2 else 128 * n)
+    i = step
+    total = bcsr + 16 * n + 24 * n
+    if i >= 2:
+        total += 8 * n * (i - 1) + 16 * n
+    if i >= 3:
+        total += 8 * n * (i - 1)
+    return total
+
+
+def _trace_from(res: N.PkResult, method: str, n: int, restart: int, nnz: int = 0) -> ExecutionTrace:
+    """ExecutionTrace filled with the launches/transfers really issued and
+    the algorithmic bytes of those kernels (so the cost model prices both
+    sides with the same terms; execmodel.py:227-278).
 
     GMRES step i of a cycle launches SpMV+normalize (i=1), SpMV+update+
     normalize (i=2) or SpMV+multi-dot+update+normalize (i>=3)."""
     tr = ExecutionTrace()
-    tr.add_phase(SETUP, res.setup_launches, res.setup_transfers, bytes_transfer=8 * 2 * n)
+    tr.add_phase(SETUP, res.setup_launches, res.setup_transfers, bytes_kernel=(12 * nnz + 48 * n) if nnz else 0,
+                 bytes_transfer=8 * 2 * n)
     for i in range(res.iterations):
         if method == "gmres":
             step = i % restart + 1
             launches = 2 if step == 1 else (3 if step == 2 else 4)
         else:
+            step = 1
             launches = res.launches_per_iteration
-        tr.add_phase(ITERATION, launches, res.transfers_per_iteration)
+        kb = iteration_kernel_bytes(method, n, nnz, launches, step) if nnz else 0
+        tr.add_phase(ITERATION, launches, res.transfers_per_iteration, bytes_kernel=kb)
     for _ in range(res.check_phases):
-        tr.add_phase(CHECK, 1, 1)
-    tr.add_phase(FINISH, res.finish_launches, res.finish_transfers, bytes_transfer=8 * (n + res.iterations))
+        tr.add_phase(CHECK, 1, 1, bytes_kernel=(12 * nnz + 24 * n) if nnz else 0, bytes_transfer=8)
+    tr.add_phase(FINISH, res.finish_launches, res.finish_transfers,
+                 bytes_kernel=(12 * nnz + 24 * n) if nnz else 0, bytes_transfer=8 * (n + res.iterations))
     return tr
 
 
@@ -233,7 +271,7 @@ def _run(method: str, a, b, x0, config, context, debug):
         dc.handle, dm.handle, N.METHODS[method], b.ctypes.data_as(dp),
         x0.ctypes.data_as(dp) if x0 is not None else None, C.byref(ncfg), _trisolve_cb, None,
         x.ctypes.data_as(dp), hist.ctypes.data_as(dp), len(hist), C.byref(res)), f"{method}_pipelined")
-    trace = _trace_from(res, method, n, cfg.restart)
+    trace = _trace_from(res, method, n, cfg.restart, dm.nnz)
     diag = {}
     if debug:
         diag["device"] = {"launches": res.total_launches, "transfers": res.total_transfers,
@@ -335,7 +373,7 @@ def solve_resident(method: str, a, b, x0=None, config=None, context=None, profil
     result = SolverResult(
         x=None, residual_history=[float(v) for v in hist[: res.iterations]],
         true_final_residual=float(res.true_final_residual), iterations=int(res.iterations),
-        termination=N.TERM_NAMES[res.termination], trace=_trace_from(res, method, n, cfg.restart),
+        termination=N.TERM_NAMES[res.termination], trace=_trace_from(res, method, n, cfg.restart, dm.nnz),
         breakdown_kind=N.KIND_NAMES[res.breakdown_kind], loop_seconds=float(res.loop_seconds),
         diagnostics={"launches": res.total_launches, "launches_per_iteration": res.launches_per_iteration,
                      "kernel_seconds": [float(v) for v in res.kernel_seconds],
@@ -354,6 +392,10 @@ def solve_batch(systems, tag=("cg", "pipelined"), config=None, context=None, thr
         tag = (tag, "pipelined")
     if tuple(tag) not in SOLVERS:
         raise ValueError(f"unknown solver {tag!r}; the B200 path implements {sorted(SOLVERS)}")
+    if tag[1] != "pipelined":
+        # the batch runs the native pipelined drivers; a classical tag would
+        # silently get different rounding and a different trace
+        raise ValueError(f"solve_batch runs the pipelined drivers only, got {tag!r}")
     method = tag[0]
     cfg = SolverConfig.coerce(config)
     if method == "gmres" and cfg.orthogonalization != CLASSICAL_GS:
@@ -393,6 +435,6 @@ def solve_batch(systems, tag=("cg", "pipelined"), config=None, context=None, thr
         out.append(SolverResult(
             x=xs[i], residual_history=[float(v) for v in hists[i][: r.iterations]],
             true_final_residual=float(r.true_final_residual), iterations=int(r.iterations),
-            termination=N.TERM_NAMES[r.termination], trace=_trace_from(r, method, mats[i].n_rows, cfg.restart),
+            termination=N.TERM_NAMES[r.termination], trace=_trace_from(r, method, mats[i].n_rows, cfg.restart, mats[i].nnz),
             breakdown_kind=N.KIND_NAMES[r.breakdown_kind], loop_seconds=float(r.loop_seconds), diagnostics={}))
     return out
