@@ -158,7 +158,7 @@ def test_spmv_fused_known_answer(pk, fused):
 
 def test_breakdown_flags(pk, fused):
     ctx = pk.ExecutionContext(1, 1)
-    with pytest.raises(fused.Breakdown):
+    with pytest.raises(fused.BreakdownError):
         fused.fused_bicgstab_s_update(dev([1.0]), dev([1.0]), dev([[1.0]]), dev([[0.0]]), ctx)
     with pytest.raises(fused.LuckyBreakdown):
         z = dev([0.0, 0.0])
