@@ -124,6 +124,28 @@ typedef struct pk_result {
 typedef int (*pk_trisolve_fn)(void* user, int64_t k, const double* R, int64_t ld,
                               const double* xi, double breakdown_tolerance, double* eta);
 
+/* Per-iteration diagnostics (the reference's debug=True side computations,
+ * solvers.py:417-467, 606-673, 895-997).  Registered on a context with
+ * pk_ctx_set_debug; while set, solves on that context run their loop from the
+ * host one iteration at a time (same kernels, same bits) and call the hook
+ * with HOST copies of the vectors the reference inspects:
+ *   PK_DBG_CG_SETUP   v0 = r after setup; scal = {beta} if the loop runs
+ *   PK_DBG_CG_ITER    v0 = r after the update; scal = {beta} unless stopping
+ *   PK_DBG_BICG_SETUP v0 = r0*
+ *   PK_DBG_BICG_S     v0 = r, v1 = Ap, scal = {alpha} (s = r - alpha Ap)
+ *   PK_DBG_BICG_XRP   v0 = r after the xrp update; scal = {identity}
+ *   PK_DBG_GMRES_CYCLE v0 = the cycle's k basis vectors, row-major k x n;
+ *                     scal = {k}
+ * Return 0 to continue.  The hook runs on the solving host thread. */
+typedef int (*pk_debug_fn)(void* user, int32_t event, int64_t iteration, const double* v0,
+                           const double* v1, int64_t n, const double* scal, int32_t nscal);
+#define PK_DBG_CG_SETUP 1
+#define PK_DBG_CG_ITER 2
+#define PK_DBG_BICG_SETUP 3
+#define PK_DBG_BICG_S 4
+#define PK_DBG_BICG_XRP 5
+#define PK_DBG_GMRES_CYCLE 6
+
 /* ---- library ---------------------------------------------------------- */
 const char* pk_last_error(void);
 int pk_abi_version(void);
@@ -133,6 +155,8 @@ int pk_device_count(int* count);
  * power of two.  Creates a non-blocking stream on `device`. */
 int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, pk_ctx** out);
 int pk_ctx_destroy(pk_ctx* ctx);
+/* hook NULL: back to device-resident loops without diagnostics */
+int pk_ctx_set_debug(pk_ctx* ctx, pk_debug_fn hook, void* user);
 /* Run kernel-level entries on `stream` (a cudaStream_t; NULL is the legacy
  * default stream, as everywhere in CUDA).  pk_ctx_reset_stream restores the
  * context's private non-blocking stream. */
@@ -163,6 +187,20 @@ int pk_csr_info(const pk_mat* mat, int64_t* n_rows, int64_t* n_cols, int64_t* nn
 int pk_csr_download(pk_ctx* ctx, const pk_mat* mat, int64_t* row_offsets, int64_t* col_indices,
                     double* values);
 int pk_mat_destroy(pk_mat* mat);
+
+/* Storage the kernels walk (the CSR arrays always stay resident):
+ *   PK_FMT_CSR     row_offsets / columns / values (thread-per-row walk);
+ *   PK_FMT_SELL32  an additional SELL-32 copy: 32-row slices, slot-major,
+ *                  padded to the slice's longest row (column -1), so a warp's
+ *                  32 rows read every slot as one coalesced segment.  Same
+ *                  entries in the same order: bit-identical results.
+ * New matrices get the context default (SELL-32 unless PK_SELL=0).
+ * Replaces nothing in the reference (its CsrMatrix is CSR only,
+ * linalg.py:71-176); it is the GPU layout of the same matrix. */
+#define PK_FMT_CSR 0
+#define PK_FMT_SELL32 1
+int pk_mat_set_format(pk_ctx* ctx, pk_mat* mat, int32_t format);
+int pk_mat_get_format(const pk_mat* mat, int32_t* format, int64_t* stored_entries);
 
 /* ---- kernel-level entries (device pointers; fused.py / linalg.py) ------ */
 /* spmv_csr (linalg.py:373-380). */
@@ -268,6 +306,15 @@ int pk_solve_batch(pk_ctx* ctx, int64_t nsys, const pk_mat* const* mats, int32_t
                    const double* const* b, const double* const* x0, const pk_config* config,
                    pk_trisolve_fn trisolve, void* trisolve_user, double* const* x_out,
                    double* const* hist_out, int64_t hist_cap, pk_result* results, int32_t nthreads);
+
+/* Launch floor of the device-resident loops: time per iteration of a
+ * conditional-WHILE graph holding `kernels_per_iteration` empty gated kernels
+ * of `grid` CTAs (<= 0: 4 per SM), each CTA taking a ticket and the last one
+ * advancing the iteration / setting the WHILE condition as a finalizer does.
+ * Best of 3 runs of `iterations`.  No reference counterpart (the reference
+ * models this as DeviceProfile.launch_latency, execmodel.py:42-107). */
+int pk_launch_floor(pk_ctx* ctx, int32_t kernels_per_iteration, int32_t grid, int64_t iterations,
+                    double* us_per_iteration);
 
 /* ---- row-partitioned CG (BASELINE configs[3]) -------- */
 /* gen_poisson3d_block(side, 1) split into `world` group-aligned z-slabs; per

@@ -775,3 +775,24 @@ def convdiff3d(side, cx=1.0, cy=1.0, cz=1.0):
     offs = [(0, -1, -1.0 - h * cx), (0, 1, -1.0), (1, -1, -1.0 - h * cy), (1, 1, -1.0),
             (2, -1, -1.0 - h * cz), (2, 1, -1.0)]
     return _stencil_csr((side, side, side), 6.0 + h * (cx + cy + cz), offs), np.ones(side ** 3)
+
+
+def poisson3d_block(side, block):
+    """gen_poisson3d_block(side, block) restated (io.py:232-275): COO triplets
+    of the 6/-1 Laplacian times I + ones/block, then lexicographic sort by
+    (row, column) -- the canonical order CsrMatrix.from_coo produces
+    (linalg.py:121-145); the triplets are unique so nothing is summed."""
+    lap = poisson3d(side, 6.0, -1.0)[0]
+    b = int(block)
+    bmat = np.eye(b) + np.ones((b, b)) / b
+    lrow = np.repeat(np.arange(lap.n_rows, dtype=np.int64), np.diff(lap.rowptr))
+    st = np.arange(b * b, dtype=np.int64)
+    rows = (np.repeat(lrow * b, b * b) + np.tile(st // b, lrow.size))
+    cols = (np.repeat(lap.cols * b, b * b) + np.tile(st % b, lrow.size))
+    vals = np.repeat(lap.vals, b * b) * np.tile(bmat.ravel(), lrow.size)
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    n = lap.n_rows * b
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rowptr[1:])
+    return Csr(n, n, rowptr, cols, vals), np.ones(n)

@@ -43,6 +43,8 @@ from .solvers import (
     bicgstab_pipelined,
     cg_pipelined,
     gmres_pipelined,
+    host_array,
+    launch_floor,
     solve,
     solve_batch,
     solve_upper_triangular,
@@ -89,5 +91,5 @@ __all__ = [
     "gen_poisson3d_block", "gmres_pipelined", "poisson2d_grid", "poisson3d_grid", "solve", "solve_batch",
     "slab_geometry", "solve_upper_triangular", "__version__", "LuckyBreakdown", "FusedReductionRequest", "dot",
     "fused_bicgstab_s_update", "fused_bicgstab_xrp_update", "fused_cg_vector_update", "fused_gs_normalize",
-    "fused_gs_stage1", "fused_gs_update", "reduce_stage1", "reduce_stage2", "spmv_csr", "spmv_fused",
+    "fused_gs_stage1", "fused_gs_update", "reduce_stage1", "reduce_stage2", "spmv_csr", "spmv_fused", "host_array", "launch_floor",
 ]

@@ -25,6 +25,7 @@ DOT_INPUT, DOT_RESULT, DOT_VECTOR = 0, 1, 2
 VEC_AXPY, VEC_AXPY2, VEC_XPAY, VEC_SCALE, VEC_ADD_SCALED, VEC_BICG_P, VEC_COPY = range(7)
 GEN = {"poisson2d": 0, "poisson3d": 1, "convdiff2d": 2, "convdiff3d": 3}
 LOOP_GRAPH, LOOP_HOST = 0, 1
+FMT_CSR, FMT_SELL32 = 0, 1
 FLAG_PROFILE = 1
 
 
@@ -66,6 +67,10 @@ class PkResult(C.Structure):
     ]
 
 
+DEBUG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                       C.c_int64, C.POINTER(C.c_double), C.c_int32)
+DBG_CG_SETUP, DBG_CG_ITER, DBG_BICG_SETUP, DBG_BICG_S, DBG_BICG_XRP, DBG_GMRES_CYCLE = 1, 2, 3, 4, 5, 6
+
 TRISOLVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_double), C.c_int64,
                           C.POINTER(C.c_double), C.c_double, C.POINTER(C.c_double))
 
@@ -81,6 +86,7 @@ SIGNATURES = {
     "pk_ctx_create": [C.c_int, C.c_int64, C.c_int64, C.POINTER(_P)],
     "pk_ctx_destroy": [_P],
     "pk_ctx_set_stream": [_P, _P],
+    "pk_ctx_set_debug": [_P, DEBUG_FN, _P],
     "pk_ctx_reset_stream": [_P],
     "pk_ctx_synchronize": [_P],
     "pk_ctx_geometry": [_P, _I64P, _I64P],
@@ -89,6 +95,8 @@ SIGNATURES = {
     "pk_csr_info": [_P, _I64P, _I64P, _I64P, _I64P],
     "pk_csr_download": [_P, _P, _I64P, _I64P, _DP],
     "pk_mat_destroy": [_P],
+    "pk_mat_set_format": [_P, _P, C.c_int32],
+    "pk_mat_get_format": [_P, C.POINTER(C.c_int32), _I64P],
     "pk_spmv": [_P, _P, _P, _P],
     "pk_spmv_fused": [_P, _P, _P, _P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(_P), _P],
     "pk_reduce_stage1": [_P, C.c_int64, C.c_int32, C.POINTER(_P), _P],
@@ -120,6 +128,7 @@ SIGNATURES = {
     "pk_dcg_solve": [_P, _DP, C.POINTER(PkConfig), _DP, _DP, C.c_int64, C.POINTER(PkResult)],
     "pk_dcg_destroy": [_P],
     "pk_debug_bench": [_P, _P, C.c_int, C.c_int, _DP],
+    "pk_launch_floor": [_P, C.c_int32, C.c_int32, C.c_int64, _DP],
 }
 _RESTYPES = {"pk_last_error": C.c_char_p}
 

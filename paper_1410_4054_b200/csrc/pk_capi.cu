@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -94,6 +95,11 @@ struct pk_ctx {
   unsigned* gtick = nullptr;      // per-group tickets [ng] + global ticket
   unsigned* ticket = nullptr;
   std::vector<pk_ctx*> workers;   // pk_solve_batch worker contexts (kept across calls)
+  void* ws_cache = nullptr;       // cached solver workspaces (pk_solvers.inc WsCache)
+  void (*ws_cache_free)(pk_ctx*) = nullptr;
+  bool ws_cache_on = true;        // PK_WS_CACHE=0 disables the workspace / graph cache
+  pk_debug_fn dbg = nullptr;      // per-iteration diagnostics hook (pk_ctx_set_debug)
+  void* dbg_user = nullptr;
   bool pdl = false;               // PK_PDL=1: programmatic stream serialization (measured slower, off)
   int mat_mink = 0;               // two-phase SpMV engine for CHAIN chains K >= mat_mink (PK_MAT_MINK=9 to try; 0 = off:
                                   // measured slower than the fused engine on C2, profiles/ENGINE_EXPERIMENTS.md)
@@ -101,16 +107,28 @@ struct pk_ctx {
   size_t mat_cap = 0;
   bool mat_discard = true;
   bool sweep_one_batch = false;   // PK_SWEEP_ONEBATCH: elementwise sweeps with one V-row batch per thread
+  bool staged = true;             // PK_STAGE=0: off (only in -DPK_STAGED_ENGINE builds: the cp.async-staged
+                                  // CHAIN engine, measured slower; compiling it in also slows the default engine)
+  bool sell_default = false;      // PK_SELL=1: new matrices also get a SELL-32 copy the kernels walk (measured slower on B200 for the stencil configs; off)
+  bool sweep_scalar = false;      // PK_SWEEP_SCALAR=1: scalar grid-stride sweeps instead of the 16-byte k_sweep2
   bool warp_k1 = true;            // PK_WARP_K1: n <= G systems on the warp chain engine (vs LEAF)        // PK_MAT_DISCARD=0: keep consumed lines in L2 (write-back on eviction)
 };
 
 struct pk_mat {
+  uint64_t uid = 0;            // unique per matrix object (workspace-cache key)
   int device = 0;
   int64_t n_rows = 0, n_cols = 0, nnz = 0, max_row = 0;
   bool row64 = false;
   void* rowptr = nullptr;
   int32_t* cols = nullptr;
   double* vals = nullptr;
+  // SELL-32 copy (pk_mat_set_format(PK_FMT_SELL32)); the kernels walk it
+  // instead of the CSR arrays when `sell` is set
+  bool sell = false;
+  int64_t sell_nnz = 0;        // padded entries
+  void* sell_ptr = nullptr;    // RowT [n_slices + 1]
+  int32_t* sell_cols = nullptr;
+  double* sell_vals = nullptr;
 };
 
 struct pk_ell {
@@ -119,6 +137,8 @@ struct pk_ell {
   int32_t* cols = nullptr;  // [width][n_rows], sentinel n_cols on padded slots
   double* vals = nullptr;
 };
+
+static int apply_default_format(pk_ctx* c, pk_mat* m);
 
 static int set_device(int dev) {
   PK_CUDA(cudaSetDevice(dev));
@@ -147,10 +167,23 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (skip && *(volatile const int32_t*)skip) return;
   const bool ing = (gate & GATE_IN_GRAPH) != 0;
   gate &= 0xff;
-  if (st && !gate_open(st, gate, ing)) return;
+  const GateVals gv = gate_load(st, gate);
   Op op = op0;
   op.scalars(sp);
-  bool last = engine_run<NQ, U>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+  if (!gate_eval(st, gate, ing, gv)) return;
+  bool last;
+#ifdef PK_STAGED_ENGINE
+  if constexpr (Op::kSpmv) {
+    if (geo.staged)
+      last = engine_chain_staged<NQ, U>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+    else
+      last = engine_run<NQ, U>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+  } else {
+    last = engine_run<NQ, U>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+  }
+#else
+  last = engine_run<NQ, U>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+#endif
   if (last && fin != FIN_NONE && st && threadIdx.x < 32) {
     // warp 0 of the last CTA; the engine's staging memory is free now
     const Geom g2 = geo;
@@ -172,9 +205,10 @@ __global__ void __launch_bounds__(32, 8)
   if (skip && *(volatile const int32_t*)skip) return;
   const bool ing = (gate & GATE_IN_GRAPH) != 0;
   gate &= 0xff;
-  if (st && !gate_open(st, gate, ing)) return;
+  const GateVals gv = gate_load(st, gate);
   Op op = op0;
   op.scalars(sp);
+  if (!gate_eval(st, gate, ing, gv)) return;
   bool last = engine_warp_chain<NQ, R>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
   if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing, smem, kWarpStage2Doubles);
 }
@@ -206,9 +240,10 @@ __global__ void __launch_bounds__(256, 4)
   if (skip && *(volatile const int32_t*)skip) return;
   const bool ing = (gate & GATE_IN_GRAPH) != 0;
   gate &= 0xff;
-  if (st && !gate_open(st, gate, ing)) return;
+  const GateVals gv = gate_load(st, gate);
   Op op = op0;
   op.scalars(sp);
+  if (!gate_eval(st, gate, ing, gv)) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += stride) {
     double c[NQ];
@@ -316,9 +351,43 @@ template <class Op>
 __global__ void __launch_bounds__(256, 4) k_sweep(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
   pdl_wait();
   pdl_trigger();
-  if (st && !gate_open(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0)) return;
+  const GateVals gv = gate_load(st, gate & 0xff);
   op.scalars(sp);
+  if (!gate_eval(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0, gv)) return;
   sweep_rows(n, op);
+}
+
+// Vectorised elementwise sweep (operators with load2/compute2: two adjacent
+// rows through 16-byte loads and stores).  Every thread owns UP row pairs
+// p, p + T, ..., all loads of a thread issued before its first compute (pair
+// indices are clamped, so every load is unconditional and the batch stays
+// together); the grid is sized so each thread runs exactly one batch.
+template <class Op, int UP>
+__global__ void __launch_bounds__(256) k_sweep2(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
+  pdl_wait();
+  pdl_trigger();
+  const GateVals gv = gate_load(st, gate & 0xff);
+  op.scalars(sp);
+  if (!gate_eval(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0, gv)) return;
+  const int64_t np = n >> 1;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += T * UP) {
+    typename Op::Item2 it[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int64_t pu = p0 + u * T;
+      op.load2((uint32_t)(2 * (pu < np ? pu : np - 1)), it[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UP; ++u)
+      if (p0 + u * T < np) op.compute2((uint32_t)(2 * (p0 + u * T)), it[u]);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    typename Op::Item it;
+    double c[1];
+    op.load((uint32_t)(n - 1), it);
+    op.compute((uint32_t)(n - 1), it, c);
+  }
 }
 
 __global__ void k_finalize(SolveState* st, int fin, int arg) {
@@ -639,6 +708,14 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
   }
   }
   size_t smem = engine_smem_bytes(geo, NQ, U);
+#ifdef PK_STAGED_ENGINE
+  if constexpr (Op::kSpmv) {
+    if (c->staged && !geo.leaf && geo.gs >= 32) {
+      geo.staged = 1;
+      smem += staged_extra_bytes(U, Op::kSlots);
+    }
+  }
+#endif
   constexpr int MINB = NQ > 8 ? 1 : (NQ > 4 ? 2 : Op::kMinBlocks);
   auto kern = k_reduce<NQ, U, MINB, Op>;
   if (smem > 200 * 1024) return fail(PK_ERR_UNSUPPORTED, "reduction geometry needs too much shared memory");
@@ -653,9 +730,28 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
   return PK_OK;
 }
 
+template <class Op, class = void>
+struct HasVec2 : std::false_type {};
+template <class Op>
+struct HasVec2<Op, std::void_t<typename Op::Item2>> : std::true_type {};
+
+#ifndef PK_SWEEP_PAIRS
+#define PK_SWEEP_PAIRS 4
+#endif
+constexpr int kSweepPairs = PK_SWEEP_PAIRS;  // row pairs per thread of k_sweep2 (2 x 16 B per stream in flight)
+
 template <class Op>
 static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp = ScalarPtrs{},
                         SolveState* st = nullptr, int gate = GATE_NONE) {
+  if constexpr (HasVec2<Op>::value) {
+    if (!c->sweep_scalar && op.aligned16()) {
+      const int64_t np = n >> 1;
+      const int64_t grid = std::max<int64_t>(1, (np + 256 * kSweepPairs - 1) / (256 * kSweepPairs));
+      PK_CUDA(launch_k(c->pdl, k_sweep2<Op, kSweepPairs>, dim3((unsigned)grid), dim3(256), 0, s, n, op, sp, st,
+                       gate));
+      return PK_OK;
+    }
+  }
   auto kern = k_sweep<Op>;
   // sweep_one_batch: one CTA per 256 x PK_SWEEP_V rows (several waves), so
   // every thread's rows are a single batch of loads in flight; otherwise the
@@ -666,9 +762,15 @@ static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Scal
   return PK_OK;
 }
 
-template <typename RowT>
-static Csr<RowT> csr_of(const pk_mat* a) {
-  return Csr<RowT>{(const RowT*)a->rowptr, a->cols, a->vals};
+template <typename RowT, bool SELL = false>
+static Csr<RowT, SELL> csr_of(const pk_mat* a) {
+  Csr<RowT, SELL> A{(const RowT*)a->rowptr, a->cols, a->vals};
+  if constexpr (SELL) {
+    A.sp = (const RowT*)a->sell_ptr;
+    A.sc = a->sell_cols;
+    A.sv = a->sell_vals;
+  }
+  return A;
 }
 
 // nnz slots per lane per pass of the SpMV tile loop: 5 (2-D 5-point rows) or
@@ -676,12 +778,12 @@ static Csr<RowT> csr_of(const pk_mat* a) {
 static inline bool wide_rows(const pk_mat* a) { return a->max_row > 5; }
 
 // SpMV with NQ fused dots; dispatch on the row index type and slot count.
-template <int NQ, typename RowT, int S>
+template <int NQ, typename RowT, int S, bool SELL = false>
 static int spmv_fused_t(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* p, double* q,
                         const int32_t* kinds, const double* const* w, double* part, int ld, int col0,
                         SolveState* st, int gate, int fin, int fin_arg) {
-  OpSpmvFused<RowT, NQ, S> op{};
-  op.A = csr_of<RowT>(a);
+  OpSpmvFused<RowT, NQ, S, SELL> op{};
+  op.A = csr_of<RowT, SELL>(a);
   op.p = p;
   op.q = q;
   for (int k = 0; k < 4; ++k) { op.kind[k] = PK_DOT_RESULT; op.w[k] = nullptr; }
@@ -702,6 +804,10 @@ static int spmv_fused_dispatch(pk_ctx* c, cudaStream_t s, const pk_mat* a, const
     if (wide_rows(a)) return spmv_fused_t<NQ, int64_t, 7>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
     return spmv_fused_t<NQ, int64_t, 5>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
   }
+  if (a->sell) {
+    if (wide_rows(a)) return spmv_fused_t<NQ, int32_t, 7, true>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+    return spmv_fused_t<NQ, int32_t, 5, true>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
+  }
   if (wide_rows(a)) return spmv_fused_t<NQ, int32_t, 7>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
   return spmv_fused_t<NQ, int32_t, 5>(c, s, a, p, q, kinds, w, part, ld, col0, st, gate, fin, fin_arg);
 }
@@ -719,12 +825,12 @@ static int spmv_fused_any(pk_ctx* c, cudaStream_t s, const pk_mat* a, const doub
   }
 }
 
-template <typename RowT, int S>
+template <typename RowT, int S, bool SELL = false>
 static int residual_t(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double* x, const double* b, double* r,
                       double* copy1, double* copy2, double* part, SolveState* st, int gate, int fin, int fin_arg,
                       int ld, int col0) {
-  OpResidual<RowT, S> op{};
-  op.A = csr_of<RowT>(a);
+  OpResidual<RowT, S, SELL> op{};
+  op.A = csr_of<RowT, SELL>(a);
   op.x = x;
   op.b = b;
   op.r = r;
@@ -740,6 +846,10 @@ static int residual_any(pk_ctx* c, cudaStream_t s, const pk_mat* a, const double
   if (a->row64) {
     if (wide_rows(a)) return residual_t<int64_t, 7>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
     return residual_t<int64_t, 5>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
+  }
+  if (a->sell) {
+    if (wide_rows(a)) return residual_t<int32_t, 7, true>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
+    return residual_t<int32_t, 5, true>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
   }
   if (wide_rows(a)) return residual_t<int32_t, 7>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
   return residual_t<int32_t, 5>(c, s, a, x, b, r, copy1, copy2, part, st, gate, fin, fin_arg, ld, col0);
@@ -802,26 +912,55 @@ static int multidot_any(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const doub
 
 template <int NB>
 static int gs_update_t(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
-                       const double* coef_dev, double* part, SolveState* st, int gate, int fin, int fin_arg) {
+                       const double* coef_dev, const double* acc_in, double* part, SolveState* st, int gate, int fin,
+                       int fin_arg) {
   OpGsUpdate<NB> op{};
   op.v = v;
   op.nb = nb;
   op.coef = coef_dev;
+  op.acc_in = acc_in;
   for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
   ScalarPtrs sp{coef_dev, nullptr, nullptr, nullptr};
   return launch_reduce<1>(c, s, n, op, sp, part, 1, 0, st, gate, nullptr, fin, fin_arg);
 }
 
+template <int NB>
+static int gs_acc_t(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* const* basis, const double* coef_dev,
+                    const double* acc_in, double* acc_out, SolveState* st, int gate) {
+  OpGsAcc<NB> op{};
+  op.nb = nb;
+  op.coef = coef_dev;
+  op.acc_in = acc_in;
+  op.acc_out = acc_out;
+  for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
+  return launch_sweep(c, s, n, op, ScalarPtrs{}, st, gate);
+}
+
+// Gram-Schmidt update over nb basis vectors: chunks of kGsChunk accumulate
+// through `acc` (an n-vector; needed only when nb > kGsChunk), the last chunk
+// subtracts the sum from v and emits the <v,v> partials.
+constexpr int kGsChunk = 32;
+
 static int gs_update_any(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
                          const double* coef_dev, double* part, SolveState* st = nullptr, int gate = GATE_NONE,
-                         int fin = FIN_NONE, int fin_arg = 0) {
-  if (nb <= 1) return gs_update_t<1>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
-  if (nb <= 2) return gs_update_t<2>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
-  if (nb <= 4) return gs_update_t<4>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
-  if (nb <= 8) return gs_update_t<8>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
-  if (nb <= 16) return gs_update_t<16>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
-  if (nb <= 32) return gs_update_t<32>(c, s, n, v, nb, basis, coef_dev, part, st, gate, fin, fin_arg);
-  return fail(PK_ERR_UNSUPPORTED, "Gram-Schmidt update supports at most 32 basis vectors (restart <= 33)");
+                         int fin = FIN_NONE, int fin_arg = 0, double* acc = nullptr) {
+  int j0 = 0;
+  const double* acc_in = nullptr;
+  while (nb - j0 > kGsChunk) {
+    if (!acc) return fail(PK_ERR_INVALID, "Gram-Schmidt update over more than 32 vectors needs an accumulator");
+    PK_TRY(gs_acc_t<kGsChunk>(c, s, n, kGsChunk, basis + j0, coef_dev + j0, acc_in, acc, st, gate));
+    acc_in = acc;
+    j0 += kGsChunk;
+  }
+  const int r = nb - j0;
+  const double* const* bb = basis + j0;
+  const double* cd = coef_dev + j0;
+  if (r <= 1) return gs_update_t<1>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
+  if (r <= 2) return gs_update_t<2>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
+  if (r <= 4) return gs_update_t<4>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
+  if (r <= 8) return gs_update_t<8>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
+  if (r <= 16) return gs_update_t<16>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
+  return gs_update_t<32>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
 }
 
 // ---------------------------------------------------------------------------
@@ -873,6 +1012,10 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e4 = getenv("PK_MAT_DISCARD")) c->mat_discard = atoi(e4) != 0;
   if (const char* e5 = getenv("PK_WARP_K1")) c->warp_k1 = atoi(e5) != 0;
   if (const char* e6 = getenv("PK_SWEEP_ONEBATCH")) c->sweep_one_batch = atoi(e6) != 0;
+  if (const char* e7 = getenv("PK_SWEEP_SCALAR")) c->sweep_scalar = atoi(e7) != 0;
+  if (const char* e8 = getenv("PK_SELL")) c->sell_default = atoi(e8) != 0;
+  if (const char* e9 = getenv("PK_STAGE")) c->staged = atoi(e9) != 0;
+  if (const char* e10 = getenv("PK_WS_CACHE")) c->ws_cache_on = atoi(e10) != 0;
   // keep freed workspace memory in the stream-ordered pool between solves
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -888,7 +1031,9 @@ extern "C" int pk_ctx_destroy(pk_ctx* c) {
   for (pk_ctx* w : c->workers) pk_ctx_destroy(w);
   c->workers.clear();
   cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->own) cudaStreamSynchronize(c->own);
+  if (c->ws_cache_free) c->ws_cache_free(c);
   if (c->scratch) cudaFree(c->scratch);
   if (c->scratch_flag) cudaFree(c->scratch_flag);
   if (c->scratch_d) cudaFree(c->scratch_d);
@@ -897,6 +1042,13 @@ extern "C" int pk_ctx_destroy(pk_ctx* c) {
   if (c->mat) cudaFree(c->mat);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
+  return PK_OK;
+}
+
+extern "C" int pk_ctx_set_debug(pk_ctx* c, pk_debug_fn hook, void* user) {
+  if (!c) return fail(PK_ERR_INVALID, "ctx is NULL");
+  c->dbg = hook;
+  c->dbg_user = user;
   return PK_OK;
 }
 
@@ -929,8 +1081,11 @@ extern "C" int pk_ctx_geometry(const pk_ctx* c, int64_t* ng, int64_t* gs) {
 // matrices
 // ---------------------------------------------------------------------------
 
+static std::atomic<uint64_t> g_mat_uid{1};
+
 static int alloc_mat(pk_ctx* c, int64_t n_rows, int64_t n_cols, int64_t nnz, pk_mat** out) {
   pk_mat* m = new pk_mat();
+  m->uid = g_mat_uid.fetch_add(1);
   m->device = c->device;
   m->n_rows = n_rows;
   m->n_cols = n_cols;
@@ -993,6 +1148,11 @@ extern "C" int pk_csr_upload(pk_ctx* c, int64_t n_rows, int64_t n_cols, const in
   if (e != cudaSuccess) {
     pk_mat_destroy(m);
     return fail(PK_ERR_CUDA, std::string("matrix upload: ") + cudaGetErrorString(e));
+  }
+  int rcf = apply_default_format(c, m);
+  if (rcf != PK_OK && rcf != PK_ERR_UNSUPPORTED) {
+    pk_mat_destroy(m);
+    return rcf;
   }
   *out = m;
   return PK_OK;
@@ -1123,6 +1283,11 @@ static int gen_stencil(pk_ctx* c, int32_t family, const int64_t* dims, int32_t n
     pk_mat_destroy(m);
     return fail(PK_ERR_CUDA, std::string("generator: ") + cudaGetErrorString(ce));
   }
+  int rcf = apply_default_format(c, m);
+  if (rcf != PK_OK && rcf != PK_ERR_UNSUPPORTED) {
+    pk_mat_destroy(m);
+    return rcf;
+  }
   *out = m;
   return PK_OK;
 }
@@ -1157,9 +1322,136 @@ extern "C" int pk_csr_download(pk_ctx* c, const pk_mat* m, int64_t* offs, int64_
   return PK_OK;
 }
 
+// ---- SELL-32 layout ---------------------------------------------------------
+
+// width (longest row) of every 32-row slice, times 32 = the slice's padded entries
+template <typename RowT>
+__global__ void k_sell_width(int64_t n, const RowT* __restrict__ rp, int64_t* __restrict__ slice_entries) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // blockDim multiple of 32
+  const int64_t len = row < n ? (int64_t)(rp[row + 1] - rp[row]) : 0;
+  unsigned long long w = (unsigned long long)len;
+  for (int o = 16; o >= 1; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
+  if ((threadIdx.x & 31) == 0 && row < n) slice_entries[row >> 5] = (int64_t)w * 32;
+}
+
+template <typename RowT>
+__global__ void k_sell_ptr(int64_t nsl, const int64_t* __restrict__ incl, RowT* __restrict__ sp) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nsl; i += (int64_t)gridDim.x * blockDim.x)
+    sp[i] = (RowT)(i == 0 ? 0 : incl[i - 1]);
+}
+
+// thread per row: slot j of row 32 s + l -> sp[s] + 32 j + l (coalesced stores)
+template <typename RowT>
+__global__ void k_sell_fill(int64_t n, const RowT* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ va, const RowT* __restrict__ sp, int32_t* __restrict__ sc,
+                            double* __restrict__ sv) {
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const RowT b = rp[row], len = rp[row + 1] - b;
+    const RowT s0 = sp[row >> 5], w = (sp[(row >> 5) + 1] - s0) >> 5;
+    const RowT base = s0 + (RowT)(row & 31);
+    for (RowT j = 0; j < w; ++j) {
+      sc[base + 32 * j] = j < len ? ci[b + j] : -1;
+      sv[base + 32 * j] = j < len ? va[b + j] : 0.0;
+    }
+  }
+}
+
+static void free_sell(pk_mat* m) {
+  if (m->sell_ptr) cudaFree(m->sell_ptr);
+  if (m->sell_cols) cudaFree(m->sell_cols);
+  if (m->sell_vals) cudaFree(m->sell_vals);
+  m->sell_ptr = nullptr;
+  m->sell_cols = nullptr;
+  m->sell_vals = nullptr;
+  m->sell = false;
+  m->sell_nnz = 0;
+}
+
+template <typename RowT>
+static int build_sell_t(pk_ctx* c, pk_mat* m) {
+  cudaStream_t s = c->stream;
+  const int64_t n = m->n_rows, nsl = (n + 31) / 32;
+  const RowT* rp = (const RowT*)m->rowptr;
+  int64_t *ent = nullptr, *incl = nullptr, *bsum = nullptr, *bsum_incl = nullptr;
+  const int64_t nblk = (nsl + 1023) / 1024;
+  PK_CUDA(cudaMalloc(&ent, std::max<int64_t>(nsl, 1) * 8));
+  PK_CUDA(cudaMalloc(&incl, std::max<int64_t>(nsl, 1) * 8));
+  PK_CUDA(cudaMalloc(&bsum, std::max<int64_t>(nblk, 1) * 8));
+  PK_CUDA(cudaMalloc(&bsum_incl, std::max<int64_t>(nblk, 1) * 8));
+  k_sell_width<RowT><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, rp, ent);
+  k_scan_block<<<(unsigned)nblk, 1024, 0, s>>>(ent, incl, nsl, bsum);
+  std::vector<int64_t> hb((size_t)nblk);
+  PK_CUDA(cudaMemcpyAsync(hb.data(), bsum, nblk * 8, cudaMemcpyDeviceToHost, s));
+  PK_CUDA(cudaStreamSynchronize(s));
+  for (int64_t i = 1; i < nblk; ++i) hb[i] += hb[i - 1];
+  const int64_t total = nblk ? hb[nblk - 1] : 0;
+  int rc = PK_OK;
+  if (!m->row64 && total >= (1ll << 31) - 1) rc = fail(PK_ERR_UNSUPPORTED, "padded SELL-32 entries overflow int32");
+  if (rc == PK_OK) {
+    PK_CUDA(cudaMemcpyAsync(bsum_incl, hb.data(), nblk * 8, cudaMemcpyHostToDevice, s));
+    k_scan_add<<<(unsigned)nblk, 1024, 0, s>>>(incl, nsl, bsum_incl);
+    cudaError_t e = cudaMalloc(&m->sell_ptr, (size_t)(nsl + 1) * sizeof(RowT) + 64);
+    if (e == cudaSuccess) e = cudaMalloc(&m->sell_cols, (size_t)total * 4 + 64);
+    if (e == cudaSuccess) e = cudaMalloc(&m->sell_vals, (size_t)total * 8 + 64);
+    if (e != cudaSuccess) {
+      rc = fail(e == cudaErrorMemoryAllocation ? PK_ERR_NOMEM : PK_ERR_CUDA,
+                std::string("SELL-32 allocation: ") + cudaGetErrorString(e));
+    } else {
+      const int g = grid_elem(c, nsl + 1, 256);
+      k_sell_ptr<RowT><<<g, 256, 0, s>>>(nsl, incl, (RowT*)m->sell_ptr);
+      k_sell_fill<RowT><<<grid_elem(c, n, 256), 256, 0, s>>>(n, rp, m->cols, m->vals, (const RowT*)m->sell_ptr,
+                                                             m->sell_cols, m->sell_vals);
+      e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = fail(PK_ERR_CUDA, std::string("SELL-32 build: ") + cudaGetErrorString(e));
+    }
+  }
+  cudaStreamSynchronize(s);
+  cudaFree(ent);
+  cudaFree(incl);
+  cudaFree(bsum);
+  cudaFree(bsum_incl);
+  if (rc != PK_OK) {
+    free_sell(m);
+    return rc;
+  }
+  m->sell_nnz = total;
+  m->sell = true;
+  return PK_OK;
+}
+
+extern "C" int pk_mat_set_format(pk_ctx* c, pk_mat* m, int32_t format) {
+  if (!c || !m) return fail(PK_ERR_INVALID, "NULL argument");
+  if (format != PK_FMT_CSR && format != PK_FMT_SELL32) return fail(PK_ERR_INVALID, "unknown matrix format");
+  PK_TRY(set_device(m->device));
+  if (format == PK_FMT_CSR) {
+    if (m->sell) {
+      PK_CUDA(cudaStreamSynchronize(c->stream));
+      free_sell(m);
+    }
+    return PK_OK;
+  }
+  if (m->sell || m->n_rows == 0) return PK_OK;
+  if (m->row64) return fail(PK_ERR_UNSUPPORTED, "SELL-32 needs nnz < 2^31 (32-bit offsets)");
+  return build_sell_t<int32_t>(c, m);
+}
+
+extern "C" int pk_mat_get_format(const pk_mat* m, int32_t* format, int64_t* stored_entries) {
+  if (!m || !format) return fail(PK_ERR_INVALID, "NULL argument");
+  *format = m->sell ? PK_FMT_SELL32 : PK_FMT_CSR;
+  if (stored_entries) *stored_entries = m->sell ? m->sell_nnz : m->nnz;
+  return PK_OK;
+}
+
+// the context's default format for new matrices (PK_SELL env, see pk_ctx)
+static int apply_default_format(pk_ctx* c, pk_mat* m) {
+  return c->sell_default ? pk_mat_set_format(c, m, PK_FMT_SELL32) : PK_OK;
+}
+
 extern "C" int pk_mat_destroy(pk_mat* m) {
   if (!m) return PK_OK;
   cudaSetDevice(m->device);
+  free_sell(m);
   if (m->rowptr) cudaFree(m->rowptr);
   if (m->cols) cudaFree(m->cols);
   if (m->vals) cudaFree(m->vals);
@@ -1424,7 +1716,11 @@ extern "C" int pk_gs_update(pk_ctx* c, int64_t n, double* v, int32_t nb, const d
     k_stage2<<<1, 32, 0, c->stream>>>(partials, c->ng, nb, nb, coeffs);
     PK_CUDA(cudaGetLastError());
   }
-  return gs_update_any(c, c->stream, n, v, nb, basis, coeffs, norm_partials);
+  double* acc = nullptr;
+  if (nb > kGsChunk) PK_CUDA(cudaMallocAsync(&acc, (size_t)std::max<int64_t>(n, 1) * 8, c->stream));
+  int rc = gs_update_any(c, c->stream, n, v, nb, basis, coeffs, norm_partials, nullptr, GATE_NONE, FIN_NONE, 0, acc);
+  if (acc) cudaFreeAsync(acc, c->stream);
+  return rc;
 }
 
 extern "C" int pk_gs_normalize(pk_ctx* c, int64_t n, double* v, const double* norm_partials, const double* r,

@@ -73,15 +73,44 @@ __device__ __forceinline__ void set_cond(SolveState* st, unsigned v, bool ing) {
   if (ing && st->use_cond) cudaGraphSetConditional(st->cond, v);
 }
 
-__device__ __forceinline__ bool gate_open(SolveState* st, int gate, bool ing) {
+// Kernel prologues load the gate word(s) and the operator's scalars in ONE
+// memory round trip: gate_load() issues the loads, the operator's scalars()
+// issues its own, and only then gate_eval() consumes the gate (a branch on
+// the gate before the scalar loads would serialise two L2 round trips in
+// front of every CTA's first data load).
+struct GateVals {
+  int32_t status;
+  int32_t lucky;
+};
+
+__device__ __forceinline__ GateVals gate_load(const SolveState* st, int gate) {
+  GateVals g{RUNNING, 0};
+  if (gate == GATE_NONE || st == nullptr) return g;
+  // L1-cached loads: the state was written by an earlier kernel (L1 is
+  // invalidated at every launch), and a per-thread L2 load of one hot line
+  // by every warp of the grid serialises in a single L2 slice (~5k requests)
+#ifdef PK_OLD_PROLOGUE
+  g.status = *(volatile const int32_t*)&st->status;
+  if (gate == GATE_GMRES) g.lucky = *(volatile const int32_t*)&st->lucky;
+#else
+  g.status = __ldg(&st->status);
+  if (gate == GATE_GMRES) g.lucky = __ldg(&st->lucky);
+#endif
+  return g;
+}
+
+__device__ __forceinline__ bool gate_eval(SolveState* st, int gate, bool ing, GateVals g) {
   if (gate == GATE_NONE || st == nullptr) return true;
-  int s = *(volatile int32_t*)&st->status;
   bool open;
-  if (gate == GATE_STOPPING) open = s == STOPPING;
-  else if (gate == GATE_GMRES) open = (s == RUNNING) && !*(volatile int32_t*)&st->lucky;
-  else open = (s == RUNNING);
+  if (gate == GATE_STOPPING) open = g.status == STOPPING;
+  else if (gate == GATE_GMRES) open = (g.status == RUNNING) && !g.lucky;
+  else open = (g.status == RUNNING);
   if (!open && gate != GATE_STOPPING && blockIdx.x == 0 && threadIdx.x == 0) set_cond(st, 0, ing);
   return open;
+}
+
+__device__ __forceinline__ bool gate_open(SolveState* st, int gate, bool ing) {
+  return gate_eval(st, gate, ing, gate_load(st, gate));
 }
 
 __device__ __forceinline__ double msqrt(double v) { return __dsqrt_rn(v); }
@@ -268,6 +297,7 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing, doub
         st->omega = om;
         st->beta = div_rn(-asr, apr);
         double ident = add_rn(sub_rn(ss, mul_rn(mul_rn(2.0, om), ass)), mul_rn(mul_rn(om, om), asas));
+        st->ident = ident;
         int clamped = ident < 0.0;
         double rr = (0.0 > ident) ? 0.0 : ident;  // Python max(ident, 0.0)
         st->clamped = clamped;
@@ -367,8 +397,21 @@ struct ScalarPtrs {
   const int32_t* par;
 };
 
+// scalars and the ping-pong parity come from the previous kernel's finalizer:
+// L1-cached loads (see gate_load)
+#ifdef PK_OLD_PROLOGUE
 __device__ __forceinline__ double ld_scalar(const double* p, double v) { return p ? __ldcg(p) : v; }
-__device__ __forceinline__ int ld_par(const int32_t* p) { return p ? *(volatile const int32_t*)p : 0; }
+#else
+__device__ __forceinline__ double ld_scalar(const double* p, double v) { return p ? __ldg(p) : v; }
+#endif
+
+// 16-byte vector access (rows i, i + 1; i even, base 16-byte aligned)
+__device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ void st2(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+__host__ __device__ inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+__device__ __forceinline__ int ld_par(const int32_t* p) { return p ? __ldg(p) : 0; }
 
 // ---------------------------------------------------------------------------
 // SpMV operators (Op::kSpmv): the engine walks the row's CSR entries, the
@@ -378,14 +421,14 @@ __device__ __forceinline__ int ld_par(const int32_t* p) { return p ? *(volatile 
 // ---------------------------------------------------------------------------
 
 // q = A p with NQ fused dots (fused.py:86-120); NQ = 0: plain spmv_csr.
-template <typename RowT_, int NQ, int S_>
+template <typename RowT_, int NQ, int S_, bool SELL_ = false>
 struct OpSpmvFused {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = 4;
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
-  Csr<RowT> A;
+  Csr<RowT, SELL_> A;
   const double* __restrict__ p;  // gather base (column index space)
   double* q;
   int32_t kind[4];
@@ -417,14 +460,14 @@ struct OpSpmvFused {
 };
 
 // r = b + (-1) A x (add_scaled, linalg.py:450-457); optional copies; <r,r>.
-template <typename RowT_, int S_>
+template <typename RowT_, int S_, bool SELL_ = false>
 struct OpResidual {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = 4;
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
-  Csr<RowT> A;
+  Csr<RowT, SELL_> A;
   const double* __restrict__ x;
   const double* __restrict__ b;
   double* r;
@@ -450,14 +493,14 @@ struct OpResidual {
 //   r' = r - a Ap;  p' = p b + r';  x += a p;  Ap' = A p';
 //   contributions [r'.r', Ap'.p', Ap'.Ap'].
 // p' at a gathered column is recomputed from (p, r, Ap) there.
-template <typename RowT_, int S_>
+template <typename RowT_, int S_, bool SELL_ = false>
 struct OpCgFused {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = 3;
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
-  Csr<RowT> A;
+  Csr<RowT, SELL_> A;
   double* x;
   double* r[2];
   double* p[2];
@@ -522,15 +565,33 @@ struct OpCgXSweep {
   double* rn_;
   double* pn_;
   struct Item { double x, r, p, ap; };
+  struct Item2 { double2 x, r, p, ap; };
   __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.x = __ldg(x + i); it.r = __ldg(rc + i); it.p = __ldg(pc + i); it.ap = __ldg(apc + i);
   }
+  __device__ __forceinline__ void upd(double xv, double r, double p, double ap, double& xn, double& rn,
+                                      double& pn) const {
+    xn = add_rn(xv, mul_rn(alpha, p));
+    rn = sub_rn(r, mul_rn(alpha, ap));
+    pn = add_rn(mul_rn(p, beta), rn);
+  }
   template <int M>
   __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&)[M]) const {
-    double xn = add_rn(it.x, mul_rn(alpha, it.p));
-    double rn = sub_rn(it.r, mul_rn(alpha, it.ap));
-    double pn = add_rn(mul_rn(it.p, beta), rn);
+    double xn, rn, pn;
+    upd(it.x, it.r, it.p, it.ap, xn, rn, pn);
     x[i] = xn; rn_[i] = rn; pn_[i] = pn;
+  }
+  __device__ __forceinline__ void load2(uint32_t i, Item2& t) const {
+    t.x = ld2(x + i); t.r = ld2(rc + i); t.p = ld2(pc + i); t.ap = ld2(apc + i);
+  }
+  __device__ __forceinline__ void compute2(uint32_t i, Item2& t) const {
+    double x0, r0, p0, x1, r1, p1;
+    upd(t.x.x, t.r.x, t.p.x, t.ap.x, x0, r0, p0);
+    upd(t.x.y, t.r.y, t.p.y, t.ap.y, x1, r1, p1);
+    st2(x + i, x0, x1); st2(rn_ + i, r0, r1); st2(pn_ + i, p0, p1);
+  }
+  bool aligned16() const {
+    return al16(x) && al16(r[0]) && al16(r[1]) && al16(p[0]) && al16(p[1]) && al16(ap[0]) && al16(ap[1]);
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
     alpha = ld_scalar(sp.a, alpha);
@@ -541,14 +602,14 @@ struct OpCgXSweep {
   }
 };
 
-template <typename RowT_, int S_>
+template <typename RowT_, int S_, bool SELL_ = false>
 struct OpCgApNext {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = 4;
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
-  Csr<RowT> A;
+  Csr<RowT, SELL_> A;
   double* r[2];
   double* p[2];
   double* ap[2];
@@ -579,14 +640,14 @@ struct OpCgApNext {
 // BiCGStab second SpMV with the s-update folded in (fused.py:154-182 + 86-120):
 //   s = r - a Ap (recomputed at every gathered column, never stored);
 //   As = A s;  contributions [s.s, As.s, As.As, As.r0*].
-template <typename RowT_, int S_>
+template <typename RowT_, int S_, bool SELL_ = false>
 struct OpBicgB {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = PK_BICGB_MINB;
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
-  Csr<RowT> A;
+  Csr<RowT, SELL_> A;
   const double* r[2];
   const double* ap[2];
   const double* __restrict__ r0;
@@ -622,7 +683,7 @@ struct OpBicgB {
 // (fused.py:185-219 + 86-120):
 //   s = r - a Ap;  x += (a p) + (w s);  r' = s - w As;  p' = ((p - w Ap) b) + r';
 //   Ap' = A p';  contributions [r'.r0*, Ap'.r0*].
-template <typename RowT_, int S_>
+template <typename RowT_, int S_, bool SELL_ = false>
 struct OpBicgA {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
@@ -630,7 +691,7 @@ struct OpBicgA {
   static constexpr int kRowsPerThread = 4;
   static constexpr int kSlots = S_;
   static constexpr int kWarpRows = 2;
-  Csr<RowT> A;
+  Csr<RowT, SELL_> A;
   double* x;
   double* r[2];
   double* p[2];
@@ -700,16 +761,34 @@ struct OpBicgXrpSweep {
   double* rn_;
   double* pn_;
   struct Item { double x, r, p, ap, as; };
+  struct Item2 { double2 x, r, p, ap, as; };
   __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.x = __ldg(x + i); it.r = __ldg(rc + i); it.p = __ldg(pc + i); it.ap = __ldg(apc + i); it.as = __ldg(as + i);
   }
+  __device__ __forceinline__ void upd(double xv, double r, double p, double ap, double asv, double& xn, double& rn,
+                                      double& pn) const {
+    double s = sub_rn(r, mul_rn(alpha, ap));
+    xn = add_rn(xv, add_rn(mul_rn(alpha, p), mul_rn(omega, s)));
+    rn = sub_rn(s, mul_rn(omega, asv));
+    pn = add_rn(mul_rn(sub_rn(p, mul_rn(omega, ap)), beta), rn);
+  }
   template <int M>
   __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&)[M]) const {
-    double s = sub_rn(it.r, mul_rn(alpha, it.ap));
-    double xn = add_rn(it.x, add_rn(mul_rn(alpha, it.p), mul_rn(omega, s)));
-    double rn = sub_rn(s, mul_rn(omega, it.as));
-    double pn = add_rn(mul_rn(sub_rn(it.p, mul_rn(omega, it.ap)), beta), rn);
+    double xn, rn, pn;
+    upd(it.x, it.r, it.p, it.ap, it.as, xn, rn, pn);
     x[i] = xn; rn_[i] = rn; pn_[i] = pn;
+  }
+  __device__ __forceinline__ void load2(uint32_t i, Item2& t) const {
+    t.x = ld2(x + i); t.r = ld2(rc + i); t.p = ld2(pc + i); t.ap = ld2(apc + i); t.as = ld2(as + i);
+  }
+  __device__ __forceinline__ void compute2(uint32_t i, Item2& t) const {
+    double x0, r0, p0, x1, r1, p1;
+    upd(t.x.x, t.r.x, t.p.x, t.ap.x, t.as.x, x0, r0, p0);
+    upd(t.x.y, t.r.y, t.p.y, t.ap.y, t.as.y, x1, r1, p1);
+    st2(x + i, x0, x1); st2(rn_ + i, r0, r1); st2(pn_ + i, p0, p1);
+  }
+  bool aligned16() const {
+    return al16(x) && al16(r[0]) && al16(r[1]) && al16(p[0]) && al16(p[1]) && al16(ap[0]) && al16(ap[1]) && al16(as);
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
     alpha = ld_scalar(sp.a, alpha);
@@ -721,14 +800,14 @@ struct OpBicgXrpSweep {
   }
 };
 
-template <typename RowT_, int S_>
+template <typename RowT_, int S_, bool SELL_ = false>
 struct OpBicgApNext {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = 4;
   static constexpr int kRowsPerThread = 2;
   static constexpr int kSlots = S_;
-  Csr<RowT> A;
+  Csr<RowT, SELL_> A;
   double* r[2];
   double* p[2];
   double* ap[2];
@@ -928,6 +1007,10 @@ struct OpMultiDot {
 };
 
 // fused_gs_update (fused.py:246-277): v -= sum_j c_j b_j; <v,v>.
+// acc = ((0 + c_0 b_0) + c_1 b_1) + ... in basis order (fused.py:268-272); a
+// basis longer than NB is accumulated in chunks (OpGsAcc) through an
+// n-vector `acc_in` -- the running sum is stored exactly, so the chunked sum
+// is the same sequence of roundings.
 template <int NB>
 struct OpGsUpdate {
   static constexpr bool kSpmv = false;
@@ -936,10 +1019,12 @@ struct OpGsUpdate {
   double* v;
   int32_t nb;
   const double* b[NB];
-  const double* coef;  // device [nb], finalized by the previous kernel
-  struct Item { double v; double b[NB]; };
+  const double* coef;    // device [nb], finalized by the previous kernel
+  const double* acc_in;  // running sum of the earlier chunks, or null (start from 0.0)
+  struct Item { double v, a; double b[NB]; };
   __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.v = v[i];
+    it.a = acc_in ? __ldg(acc_in + i) : 0.0;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       it.b[j] = 0.0;
@@ -948,16 +1033,46 @@ struct OpGsUpdate {
   }
   template <int M>
   __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&cc)[M]) const {
-    double acc = 0.0;
+    double acc = it.a;
 #pragma unroll
     for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(__ldg(coef + j), it.b[j]));
-    double vn = nb > 0 ? sub_rn(it.v, acc) : it.v;
+    double vn = (nb > 0 || acc_in) ? sub_rn(it.v, acc) : it.v;
     v[i] = vn;
     cc[0] = mul_rn(vn, vn);
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
     if (sp.a) coef = sp.a;
   }
+};
+
+// A leading chunk of the Gram-Schmidt accumulation (no reduction):
+// acc_out = acc_in (or 0.0) + sum_j c_j b_j over this chunk, in order.
+template <int NB>
+struct OpGsAcc {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = NB > 8 ? 2 : 4;
+  int32_t nb;
+  const double* b[NB];
+  const double* coef;
+  const double* acc_in;
+  double* acc_out;
+  struct Item { double a; double b[NB]; };
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
+    it.a = acc_in ? __ldg(acc_in + i) : 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      it.b[j] = 0.0;
+      if (j < nb) it.b[j] = __ldg(b[j] + i);
+    }
+  }
+  template <int M>
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&)[M]) const {
+    double acc = it.a;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(__ldg(coef + j), it.b[j]));
+    acc_out[i] = acc;
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs&) {}
 };
 
 // fused_gs_normalize (fused.py:280-305): v *= inv; <r, v>.

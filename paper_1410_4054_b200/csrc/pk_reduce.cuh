@@ -70,6 +70,7 @@ struct Geom {
   int32_t tT;      // CHAIN group tree: threads = min(gs, kThreads)
   int32_t tm;      // CHAIN group tree: leaves per tree thread
   int32_t tlogm;
+  int32_t staged;  // CHAIN + SpMV operator: engine_chain_staged (column indices staged by cp.async)
 };
 
 // min_units: LEAF groups are split over F = 2^logf CTAs (each a contiguous
@@ -126,14 +127,40 @@ struct Scratch {
   unsigned* ticket;   // global ticket (kernel-level entries; solvers use SolveState)
 };
 
-// CSR triple on the device.
-template <typename RowT_>
+// CSR triple on the device, optionally with a SELL-32 copy of the same
+// entries (sp != nullptr): rows are cut into slices of 32 consecutive rows,
+// slice s holds its rows' entries slot-major -- slot j of row 32 s + l at
+// sp[s] + 32 j + l, the slice padded to its longest row with column -1 (and
+// value 0) -- so the 32 lanes of a warp walking 32 aligned rows read slot j
+// as one 128-byte (columns) / 256-byte (values) segment instead of 32
+// stride-5 scattered words, and need one row-bounds load per warp (sp[s],
+// sp[s + 1]) instead of one per row.  Entries keep their stored order, so
+// the row sums (and every bit of the result) are those of the CSR loop.
+template <typename RowT_, bool SELL_ = false>
 struct Csr {
   using RowT = RowT_;
+  static constexpr bool kSell = SELL_;  // walk the SELL-32 copy (compile-time: the CSR code stays as lean as before)
   const RowT* rp;
   const int32_t* ci;
   const double* va;
+  const RowT* sp = nullptr;   // SELL-32 slice offsets (entries), n_slices + 1
+  const int32_t* sc = nullptr;
+  const double* sv = nullptr;
 };
+
+// [b, e) walk of a row and the slot stride: CSR (rp[row], rp[row + 1], 1) or
+// SELL-32 (sp[s] + lane, sp[s + 1], 32).
+template <typename RowT, bool SELL>
+__device__ __forceinline__ void row_span(const Csr<RowT, SELL>& A, uint32_t row, RowT& b, RowT& e) {
+  if constexpr (SELL) {
+    const uint32_t sl = row >> 5;
+    b = __ldg(A.sp + sl) + (RowT)(row & 31u);
+    e = __ldg(A.sp + sl + 1);
+  } else {
+    b = __ldg(A.rp + row);
+    e = __ldg(A.rp + row + 1);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // phase A: the contributions of one row (lean thread-per-row code)
@@ -170,23 +197,28 @@ __device__ __forceinline__ void row_contrib(const Op& op, uint32_t row, double (
     using RowT = typename Op::RowT;
     constexpr int S = Op::kSlots;
     const bool have = rb_pre <= re_pre;
-    const RowT b = have ? rb_pre : __ldg(op.A.rp + row), e = have ? re_pre : __ldg(op.A.rp + row + 1);
+    RowT b = rb_pre, e = re_pre;
+    if (!have) row_span(op.A, row, b, e);
+    constexpr bool sell = std::decay_t<decltype(op.A)>::kSell;
+    const RowT st = sell ? 32 : 1;
+    const int32_t* __restrict__ ci = sell ? op.A.sc : op.A.ci;
+    const double* __restrict__ va = sell ? op.A.sv : op.A.va;
     double acc = 0.0;
-    for (RowT k0 = b; k0 < e; k0 += S) {
+    for (RowT k0 = b; k0 < e; k0 += S * st) {
       int32_t col[S];
       double val[S];
       typename Op::Gat gv[S];
 #pragma unroll
       for (int j = 0; j < S; ++j) {
-        const RowT k = (k0 + j < e) ? k0 + j : e - 1;
-        col[j] = __ldg(op.A.ci + k);
-        val[j] = __ldg(op.A.va + k);
+        const RowT k = (k0 + j * st < e) ? k0 + j * st : b;  // past the end: re-read a valid slot
+        col[j] = __ldg(ci + k);
+        val[j] = __ldg(va + k);
       }
 #pragma unroll
-      for (int j = 0; j < S; ++j) op.gload((uint32_t)col[j], gv[j]);
+      for (int j = 0; j < S; ++j) op.gload((uint32_t)(col[j] < 0 ? 0 : col[j]), gv[j]);
 #pragma unroll
       for (int j = 0; j < S; ++j)
-        if (k0 + j < e) acc = add_rn(acc, mul_rn(val[j], op.gval(gv[j])));
+        if (k0 + j * st < e && col[j] >= 0) acc = add_rn(acc, mul_rn(val[j], op.gval(gv[j])));
     }
     op.compute(row, it, acc, c);
   } else {
@@ -375,10 +407,7 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
             const int64_t rn = kn * geo.G + lid0 + lane;
             nb[u] = 1;
             ne[u] = 0;
-            if (kn < geo.K && lane_ok && rn < geo.n) {
-              nb[u] = __ldg(op.A.rp + rn);
-              ne[u] = __ldg(op.A.rp + rn + 1);
-            }
+            if (kn < geo.K && lane_ok && rn < geo.n) row_span(op.A, (uint32_t)rn, nb[u], ne[u]);
           }
         }
         __syncthreads();
@@ -544,6 +573,202 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
   return s_last != 0;
 }
 
+// ---------------------------------------------------------------------------
+// CHAIN engine with staged column indices (SpMV operators)
+// ---------------------------------------------------------------------------
+//
+// Same mapping, fold order, spill / ticket / group-tree protocol as the CHAIN
+// branch of engine_run(); what changes is how a row's inputs arrive.  The
+// column indices of the first pass (kSlots entries) of every row of batch
+// t + 1 are copied global -> shared with cp.async (4-byte LDGSTS, zero-fill
+// past the row end: no registers held, no read) while batch t folds, and the
+// row bounds are loaded two batches ahead; the CTA's batches are one
+// flattened stream across its units, so the pipeline does not drain at unit
+// boundaries.  A batch's critical path is then shared-memory columns ->
+// gathers (values and the row's own vectors load beside the gathers) instead
+// of row bounds -> columns -> gathers.  Same contributions, same order: the
+// same bits.
+
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(gsrc), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__host__ __device__ inline size_t staged_extra_bytes(int U, int S) { return (size_t)U * S * kThreads * 4; }
+
+// Row contribution with the first pass's columns taken from shared memory
+// (cs[j * kThreads], this thread's slots); longer rows continue from global.
+template <int NQ, class Op>
+__device__ __forceinline__ void row_contrib_staged(const Op& op, uint32_t row, double (&c)[NQ],
+                                                   typename Op::RowT b, typename Op::RowT e, const int32_t* cs) {
+  using RowT = typename Op::RowT;
+  constexpr int S = Op::kSlots;
+  typename Op::Item it;
+  op.load(row, it);
+  constexpr bool sell = std::decay_t<decltype(op.A)>::kSell;
+  const RowT st = sell ? 32 : 1;
+  const int32_t* __restrict__ ci = sell ? op.A.sc : op.A.ci;
+  const double* __restrict__ va = sell ? op.A.sv : op.A.va;
+  double acc = 0.0;
+  for (RowT k0 = b; k0 < e; k0 += S * st) {
+    int32_t col[S];
+    double val[S];
+    typename Op::Gat gv[S];
+    const bool first = k0 == b;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const RowT k = (k0 + j * st < e) ? k0 + j * st : b;
+      col[j] = first ? cs[j * kThreads] : __ldg(ci + k);
+      val[j] = __ldg(va + k);
+    }
+#pragma unroll
+    for (int j = 0; j < S; ++j) op.gload((uint32_t)(col[j] < 0 ? 0 : col[j]), gv[j]);
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (k0 + j * st < e && col[j] >= 0) acc = add_rn(acc, mul_rn(val[j], op.gval(gv[j])));
+  }
+  op.compute(row, it, acc, c);
+}
+
+// row of batch t (of this CTA's flattened (unit, batch) stream), slot u of this thread, or -1
+__device__ __forceinline__ int64_t staged_row(const Geom& geo, int64_t T, int64_t nbpu, int B, int64_t t, int u,
+                                             int warp, int lane) {
+  if (t >= T) return -1;
+  const int64_t unit = (int64_t)blockIdx.x + (t / nbpu) * gridDim.x;
+  const int64_t k = (t % nbpu) * B + warp + kWarps * u;
+  const int64_t lid0 = unit * 32;
+  if (k >= geo.K || lid0 + lane >= geo.G) return -1;
+  const int64_t row = k * geo.G + lid0 + lane;
+  return row < geo.n ? row : -1;
+}
+
+template <int NQ, int U, class Op>
+__device__ __forceinline__ bool engine_chain_staged(const Geom& geo, const Op& op, double* smem, double* part, int ld,
+                                                    int col0, int nstore, const Scratch& scr, unsigned* ticket) {
+  using RowT = typename Op::RowT;
+  constexpr int S = Op::kSlots;
+  __shared__ int s_flag;
+  __shared__ int s_last;
+  constexpr int B = kWarps * U;
+  constexpr int QPW = (NQ + kWarps - 1) / kWarps;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  double* Cbuf = smem;  // [2][B][NQ][32]
+  double* tail = Cbuf + 2 * B * NQ * 32;
+  int32_t* cst = reinterpret_cast<int32_t*>(tail + engine_tail_doubles(geo, NQ));  // [U][S][kThreads]
+  if (tid == 0) s_last = 0;
+  constexpr bool sell = std::decay_t<decltype(op.A)>::kSell;
+  const RowT st = sell ? 32 : 1;
+  const int32_t* __restrict__ ci = sell ? op.A.sc : op.A.ci;
+  const int64_t nbpu = (geo.K + B - 1) / B;  // batches per unit
+  const int64_t my_units =
+      geo.units > (int64_t)blockIdx.x ? (geo.units - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t T = my_units * nbpu;
+#define PK_STG_BOUNDS(t_, bb, ee)                                                   \
+  _Pragma("unroll") for (int u = 0; u < U; ++u) {                                   \
+    bb[u] = 1;                                                                      \
+    ee[u] = 0;                                                                      \
+    const int64_t r_ = staged_row(geo, T, nbpu, B, (t_), u, warp, lane);            \
+    if (r_ >= 0) row_span(op.A, (uint32_t)r_, bb[u], ee[u]);                        \
+  }
+#define PK_STG_STAGE(bb, ee)                                                        \
+  _Pragma("unroll") for (int u = 0; u < U; ++u) {                                   \
+    _Pragma("unroll") for (int j = 0; j < S; ++j) {                                 \
+      const RowT k_ = bb[u] + j * st;                                               \
+      const bool v_ = bb[u] <= ee[u] && k_ < ee[u];                                 \
+      cp_async4(cst + (u * S + j) * kThreads + tid, v_ ? ci + k_ : ci, v_);         \
+    }                                                                               \
+  }                                                                                 \
+  cp_async_commit();
+  RowT cb[U], ce[U], nb[U], ne[U], fb[U], fe[U];
+  PK_STG_BOUNDS(0, cb, ce)
+  PK_STG_BOUNDS(1, nb, ne)
+  PK_STG_STAGE(cb, ce)
+  double acc[QPW];
+#pragma unroll
+  for (int i = 0; i < QPW; ++i) acc[i] = 0.0;
+  for (int64_t t = 0; t < T; ++t) {
+    PK_STG_BOUNDS(t + 2, fb, fe)
+    cp_async_wait_all();
+    double* C = Cbuf + (t & 1) * (B * NQ * 32);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = warp + kWarps * u;
+      const int64_t row = staged_row(geo, T, nbpu, B, t, u, warp, lane);
+      double c[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) c[q] = 0.0;
+      if (row >= 0) row_contrib_staged<NQ>(op, (uint32_t)row, c, cb[u], ce[u], cst + u * S * kThreads + tid);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) C[(kk * NQ + q) * 32 + lane] = c[q];
+    }
+    PK_STG_STAGE(nb, ne)
+    __syncthreads();
+    const int64_t unit = (int64_t)blockIdx.x + (t / nbpu) * gridDim.x;
+    const int64_t k0 = (t % nbpu) * B;
+    const int kend = (int)((geo.K - k0) < B ? (geo.K - k0) : B);
+#pragma unroll
+    for (int i = 0; i < QPW; ++i) {
+      const int q = warp + kWarps * i;
+      if (q < NQ) {
+        double v[B];
+#pragma unroll
+        for (int kk = 0; kk < B; ++kk) v[kk] = C[(kk * NQ + q) * 32 + lane];
+#pragma unroll
+        for (int kk = 0; kk < B; ++kk)
+          if (kk < kend) acc[i] = add_rn(acc[i], v[kk]);
+      }
+    }
+    if (t % nbpu == nbpu - 1) {
+      // ---- unit epilogue: lane values -> spill, group ticket / tree, global ticket ----
+      const int64_t lid0 = unit * 32;
+      const int nl = (int)((geo.G - lid0) < 32 ? (geo.G - lid0) : 32);
+      if (lane < nl) {
+#pragma unroll
+        for (int i = 0; i < QPW; ++i) {
+          const int q = warp + kWarps * i;
+          if (q < NQ && q < nstore) scr.spill[(int64_t)q * geo.G + lid0 + lane] = acc[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < QPW; ++i) acc[i] = 0.0;
+      __syncthreads();
+      const int g = (int)(lid0 / geo.gs);
+      if (tid == 0) {
+        const unsigned per = (unsigned)(geo.gs / 32);
+        unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
+        int last = (tk == per - 1);
+        if (last) scr.gtick[g] = 0u;
+        s_flag = last;
+      }
+      __syncthreads();
+      if (s_flag) {
+        group_tree<NQ>(geo, g, scr.spill, tail, part, ld, col0, nstore);
+        if (tid == 0) {
+          unsigned tk = atomic_add_acq_rel(ticket, 1u);
+          if (tk + 1u == (unsigned)geo.n_groups) {
+            *ticket = 0u;
+            s_last = 1;
+          }
+        }
+        __syncthreads();
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cb[u] = nb[u]; ce[u] = ne[u];
+      nb[u] = fb[u]; ne[u] = fe[u];
+    }
+  }
+#undef PK_STG_BOUNDS
+#undef PK_STG_STAGE
+  cp_async_wait_all();
+  __syncthreads();
+  return s_last != 0;
+}
+
 // Warp-level halving tree of group g over its gs (>= 32) spilled lane values:
 // lane l owns the lanes {l + 32 j}, visited in bit-reversed order of j
 // through a binary-counter stack (stk: (log2(gs/32)+1) x NQ x 32 doubles),
@@ -617,11 +842,18 @@ __device__ __forceinline__ void rows_contrib(const Op& op, const Geom& geo, int6
     using RowT = typename Op::RowT;
     constexpr int S = Op::kSlots;
     RowT b[R], e[R];
+    constexpr bool sell = std::decay_t<decltype(op.A)>::kSell;
+    const RowT st = sell ? 32 : 1;
+    const int32_t* __restrict__ ci = sell ? op.A.sc : op.A.ci;
+    const double* __restrict__ va = sell ? op.A.sv : op.A.va;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      b[r] = ok[r] ? __ldg(op.A.rp + row[r]) : (RowT)0;
-      e[r] = ok[r] ? __ldg(op.A.rp + row[r] + 1) : (RowT)0;
-      if (ok[r]) op.load(row[r], it[r]);
+      b[r] = 0;
+      e[r] = 0;
+      if (ok[r]) {
+        row_span(op.A, row[r], b[r], e[r]);
+        op.load(row[r], it[r]);
+      }
     }
     // first S entries of every row: all loads in flight, then the ordered adds
     int32_t col[R][S];
@@ -631,27 +863,29 @@ __device__ __forceinline__ void rows_contrib(const Op& op, const Geom& geo, int6
     for (int r = 0; r < R; ++r) {
 #pragma unroll
       for (int j = 0; j < S; ++j) {
-        const RowT k = (b[r] + j < e[r]) ? b[r] + j : (e[r] > b[r] ? e[r] - 1 : b[r]);
+        const RowT k = (b[r] + j * st < e[r]) ? b[r] + j * st : b[r];
         const bool live = e[r] > b[r];
-        col[r][j] = live ? __ldg(op.A.ci + k) : 0;
-        val[r][j] = live ? __ldg(op.A.va + k) : 0.0;
+        col[r][j] = live ? __ldg(ci + k) : 0;
+        val[r][j] = live ? __ldg(va + k) : 0.0;
       }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int j = 0; j < S; ++j) op.gload((uint32_t)col[r][j], gv[r][j]);
+      for (int j = 0; j < S; ++j) op.gload((uint32_t)(col[r][j] < 0 ? 0 : col[r][j]), gv[r][j]);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       double acc = 0.0;
 #pragma unroll
       for (int j = 0; j < S; ++j)
-        if (b[r] + j < e[r]) acc = add_rn(acc, mul_rn(val[r][j], op.gval(gv[r][j])));
+        if (b[r] + j * st < e[r] && col[r][j] >= 0) acc = add_rn(acc, mul_rn(val[r][j], op.gval(gv[r][j])));
       // rows longer than S: the rest in order, straight from memory
-      for (RowT k = b[r] + S; k < e[r]; ++k) {
+      for (RowT k = b[r] + S * st; k < e[r]; k += st) {
+        const int32_t cj = __ldg(ci + k);
+        if (cj < 0) continue;
         typename Op::Gat g;
-        op.gload((uint32_t)__ldg(op.A.ci + k), g);
-        acc = add_rn(acc, mul_rn(__ldg(op.A.va + k), op.gval(g)));
+        op.gload((uint32_t)cj, g);
+        acc = add_rn(acc, mul_rn(__ldg(va + k), op.gval(g)));
       }
       if (ok[r]) op.compute(row[r], it[r], acc, c[r]);
     }

@@ -42,6 +42,7 @@ struct SolveState {
   double ss, ass, asas, asr, apr, rho0;
   double nrm, inv;    // GMRES normalisation
   double dotv;        // generic finalized dot / true residual squared
+  double ident;       // BiCGStab: residual identity before the clamp (debug diagnostics)
   double rho;         // GMRES cycle residual norm
 
   unsigned int ticket;

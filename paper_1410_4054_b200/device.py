@@ -103,6 +103,29 @@ class DeviceMatrix:
             cf.ctypes.data_as(C.POINTER(C.c_double)), len(coef), C.byref(h)), "pk_csr_generate")
         return cls(h, dc.device)
 
+    FORMATS = {"csr": N.FMT_CSR, "sell32": N.FMT_SELL32}
+
+    @property
+    def format(self) -> str:
+        f = C.c_int32()
+        N.check(N.lib().pk_mat_get_format(self.handle, C.byref(f), None))
+        return {v: k for k, v in self.FORMATS.items()}[f.value]
+
+    @property
+    def stored_entries(self) -> int:
+        f, e = C.c_int32(), C.c_int64()
+        N.check(N.lib().pk_mat_get_format(self.handle, C.byref(f), C.byref(e)))
+        return e.value
+
+    def set_format(self, fmt: str, context=None) -> "DeviceMatrix":
+        """Storage the kernels walk: "csr" or "sell32" (an additional SELL-32
+        copy, slot-major 32-row slices; bit-identical results)."""
+        if fmt not in self.FORMATS:
+            raise ValueError(f"unknown matrix format {fmt!r}; expected one of {sorted(self.FORMATS)}")
+        dc = context_for(ExecutionContext(device=self.device) if context is None else context)
+        N.check(N.lib().pk_mat_set_format(dc.handle, self.handle, self.FORMATS[fmt]), "pk_mat_set_format")
+        return self
+
     def download(self, dc: DeviceContext) -> CsrMatrix:
         offs = np.empty(self.n_rows + 1, dtype=np.int64)
         cols = np.empty(self.nnz, dtype=np.int64)

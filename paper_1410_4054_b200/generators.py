@@ -97,10 +97,53 @@ def poisson3d_grid(side: int, device: bool = False, context=None):
     return _assemble((side, side, side), diag, faces), np.ones(side ** 3)
 
 
+def _block_expand(scalar: CsrMatrix, block: int) -> CsrMatrix:
+    """Kronecker product of a scalar CSR operator with the SPD block
+    B = I + ones(block, block) / block (io.py:232-275): scalar entry (i, j, v)
+    becomes the block-row entries (i b + s, j b + t, v * B[s, t]).  Every
+    block row keeps the scalar row's column order (neighbour j ascending,
+    then t), which is the canonical order from_coo would produce; no
+    duplicates arise, so no value is summed."""
+    b = int(block)
+    bmat = np.eye(b) + np.ones((b, b)) / b
+    offs, cols, vals = scalar.row_offsets, scalar.col_indices, scalar.values
+    n = scalar.n_rows
+    rowlen = np.diff(offs)
+    row_of = np.repeat(np.arange(n, dtype=np.int64), rowlen)
+    k_of = np.arange(offs[-1], dtype=np.int64) - offs[row_of]
+    t = np.arange(b, dtype=np.int64)
+    out_cols = np.empty(int(offs[-1]) * b * b, dtype=np.int64)
+    out_vals = np.empty(int(offs[-1]) * b * b)
+    for s in range(b):
+        # block row (i, s) starts at offs[i] b^2 + s rowlen_i b; entry k, column t at + k b + t
+        base = offs[row_of] * b * b + s * rowlen[row_of] * b + k_of * b
+        pos = base[:, None] + t[None, :]
+        out_cols[pos] = cols[:, None] * b + t[None, :]
+        out_vals[pos] = vals[:, None] * bmat[s][None, :]
+    out_offs = np.zeros(n * b + 1, dtype=np.int64)
+    np.cumsum(np.repeat(rowlen * b, b), out=out_offs[1:])
+    return CsrMatrix(n * b, n * b, out_offs, out_cols, out_vals)
+
+
 def gen_poisson3d_block(n: int, block: int, device: bool = False, context=None):
-    if block != 1:
-        raise NotImplementedError("the B200 path generates block == 1 (the C4 configuration) only")
-    return poisson3d_grid(n, device=device, context=context)
+    """Seven-point Laplacian (6 / -1) on an n^3 grid, every entry times the
+    block I + ones(block, block)/block (io.py:232-275); block == 1 gives the
+    12 / -2 operator of the C4 config (also generated directly in HBM with
+    ``device=True``)."""
+    if n < 1:
+        raise ValueError("grid dimension n must be at least 1")
+    if block < 1:
+        raise ValueError("block size must be at least 1")
+    if block == 1:
+        return poisson3d_grid(n, device=device, context=context)
+    faces = [(ax, st, -1.0) for ax in (0, 1, 2) for st in (-1, 1)]
+    a = _block_expand(_assemble((n, n, n), 6.0, faces), block)
+    if device:
+        from .device import device_matrix
+        from .linalg import ExecutionContext
+
+        return device_matrix(a, ExecutionContext.coerce(context)), np.ones(n ** 3 * block)
+    return a, np.ones(n ** 3 * block)
 
 
 def convdiff2d(side: int, c=(1.0, 1.0), device: bool = False, context=None):

@@ -179,6 +179,55 @@ def _trisolve_cb(user, k, rptr, ld, xiptr, btol, etaptr):
         return 1
 
 
+class _Diagnostics:
+    """The reference's debug=True side computations (solvers.py:417-467,
+    606-673, 895-997), evaluated with NumPy on host copies of the device
+    vectors the native loop hands over one iteration at a time -- the same
+    np.dot / np.linalg.norm / matmul calls on bit-identical vectors."""
+
+    def __init__(self, method: str):
+        self.method = method
+        if method == "cg":
+            self.diag = {"rr_direct": [], "beta": []}
+        elif method == "bicgstab":
+            self.diag = {"s_dot_r0star": [], "s_norm": [], "identity_rr": [], "direct_rr": []}
+        else:
+            self.diag = {"ortho_offdiag": []}
+        self.r0star = None
+        self.error = None
+
+    def __call__(self, user, event, it, v0, v1, n, scal, nscal):
+        try:
+            a0 = np.ctypeslib.as_array(v0, shape=(n,)).copy() if v0 and event != N.DBG_GMRES_CYCLE else None
+            sc = [float(scal[i]) for i in range(nscal)]
+            d = self.diag
+            if event == N.DBG_CG_SETUP or event == N.DBG_CG_ITER:
+                d["rr_direct"].append(float(np.dot(a0, a0)))
+                if sc:
+                    d["beta"].append(sc[0])
+            elif event == N.DBG_BICG_SETUP:
+                self.r0star = a0
+                d["r0star_norm"] = float(np.linalg.norm(a0))
+            elif event == N.DBG_BICG_S:
+                ap = np.ctypeslib.as_array(v1, shape=(n,))
+                s_vec = a0 - sc[0] * ap  # fused.py:177, s = r - alpha Ap
+                d["s_dot_r0star"].append(float(np.dot(s_vec, self.r0star)))
+                d["s_norm"].append(float(np.linalg.norm(s_vec)))
+            elif event == N.DBG_BICG_XRP:
+                d["identity_rr"].append(sc[0])
+                d["direct_rr"].append(float(np.dot(a0, a0)))
+            elif event == N.DBG_GMRES_CYCLE:
+                k = int(sc[0])
+                v = np.ctypeslib.as_array(v0, shape=(k * n,)).reshape(k, n)
+                vmat = np.stack([v[j].copy() for j in range(k)], axis=1)
+                gram = vmat.T @ vmat
+                d["ortho_offdiag"].append(float(np.abs(gram - np.eye(k)).max()))
+            return 0
+        except Exception as exc:  # surfaced after the native call returns
+            self.error = exc
+            return 1
+
+
 def _prepare(a, b, x0):
     """Validation of solvers.py:259-269 (ValueError on misuse)."""
     if isinstance(a, DeviceMatrix):
@@ -191,6 +240,27 @@ def _prepare(a, b, x0):
     b = np.ascontiguousarray(as_vector(b, n=n_rows, name="b"), dtype=np.float64)
     x0 = None if x0 is None else np.ascontiguousarray(as_vector(x0, n=n_rows, name="x0"), dtype=np.float64)
     return a, b, x0
+
+
+def _host_empty(n: int) -> np.ndarray:
+    """float64 host buffer for a solution: page-locked (torch's caching pinned
+    allocator, so repeated solves reuse the same blocks) when a CUDA device is
+    present -- the device->host copy of x then runs at full DMA speed; a
+    plain NumPy array otherwise."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.empty(max(n, 1), dtype=torch.float64, pin_memory=True).numpy()[:n]
+    except Exception:
+        pass
+    return np.empty(n)
+
+
+def host_array(n: int) -> np.ndarray:
+    """A float64 host vector in page-locked memory, for right-hand sides that
+    are streamed to the device every solve (full-speed DMA); see _host_empty."""
+    return _host_empty(n)
 
 
 def _native_config(cfg: SolverConfig) -> N.PkConfig:
@@ -261,21 +331,29 @@ def _run(method: str, a, b, x0, config, context, debug):
     dm = device_matrix(a, ctx)
     n = dm.n_rows
     limit = cfg.iteration_limit()
-    x = np.empty(n)
+    x = _host_empty(n)
     hist = np.empty(max(limit, 1))
     res = N.PkResult()
     ncfg = _native_config(cfg)
     dp = C.POINTER(C.c_double)
     dc.reset_stream()
-    N.check(N.lib().pk_solve(
-        dc.handle, dm.handle, N.METHODS[method], b.ctypes.data_as(dp),
-        x0.ctypes.data_as(dp) if x0 is not None else None, C.byref(ncfg), _trisolve_cb, None,
-        x.ctypes.data_as(dp), hist.ctypes.data_as(dp), len(hist), C.byref(res)), f"{method}_pipelined")
-    trace = _trace_from(res, method, n, cfg.restart, dm.nnz)
-    diag = {}
+    dbg = _Diagnostics(method) if debug else None
+    hook = N.DEBUG_FN(dbg) if debug else None
     if debug:
-        diag["device"] = {"launches": res.total_launches, "transfers": res.total_transfers,
-                          "cycles": res.cycles, "check_phases": res.check_phases}
+        N.check(N.lib().pk_ctx_set_debug(dc.handle, hook, None))
+    try:
+        rc = N.lib().pk_solve(
+            dc.handle, dm.handle, N.METHODS[method], b.ctypes.data_as(dp),
+            x0.ctypes.data_as(dp) if x0 is not None else None, C.byref(ncfg), _trisolve_cb, None,
+            x.ctypes.data_as(dp), hist.ctypes.data_as(dp), len(hist), C.byref(res))
+    finally:
+        if debug:
+            N.lib().pk_ctx_set_debug(dc.handle, N.DEBUG_FN(), None)
+    if dbg is not None and dbg.error is not None:
+        raise dbg.error
+    N.check(rc, f"{method}_pipelined")
+    trace = _trace_from(res, method, n, cfg.restart, dm.nnz)
+    diag = dbg.diag if debug else {}
     return SolverResult(
         x=x,
         residual_history=[float(v) for v in hist[: res.iterations]],
@@ -438,3 +516,17 @@ def solve_batch(systems, tag=("cg", "pipelined"), config=None, context=None, thr
             termination=N.TERM_NAMES[r.termination], trace=_trace_from(r, method, mats[i].n_rows, cfg.restart, mats[i].nnz),
             breakdown_kind=N.KIND_NAMES[r.breakdown_kind], loop_seconds=float(r.loop_seconds), diagnostics={}))
     return out
+
+
+def launch_floor(context=None, kernels_per_iteration: int = 1, grid: int = 0, iterations: int = 2000) -> dict:
+    """Measured floor of the device-resident loop: microseconds per iteration
+    of a conditional-WHILE graph with `kernels_per_iteration` empty gated
+    full-width kernels (ticket + WHILE-condition protocol of the solvers)."""
+    ctx = ExecutionContext.coerce(context)
+    dc = context_for(ctx)
+    us = C.c_double()
+    N.check(N.lib().pk_launch_floor(dc.handle, int(kernels_per_iteration), int(grid), int(iterations),
+                                    C.byref(us)), "pk_launch_floor")
+    return {"us_per_iteration": us.value, "kernels_per_iteration": kernels_per_iteration,
+            "note": f"{kernels_per_iteration} empty gated kernel(s) of {grid or '4 x SM'} CTAs per iteration in the "
+                    "unrolled conditional-WHILE graph, ticket + condition as in the solver finalizers"}

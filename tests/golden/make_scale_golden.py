@@ -26,10 +26,12 @@ as its own CsrMatrix.  Cases (VERDICT r1 "next" item 1):
   c4_256_fixed30_slab CG 3D Poisson 256^3, 30 fixed iterations, 256 x 65536
   c3_128_fixed31      GMRES(30) conv-diff 3D 128^3, 31 fixed steps (one full
                       cycle: trisolve, x update, restart), 128 x 256
+  c3_64_tol / c3_128_tol  GMRES(30) conv-diff 3D to tol 1e-8 (cycle ends with the
+                      true-residual gate), 128 x 256
   c2_1024_tol         BiCGStab conv-diff 2D 1024^2 to tol 1e-8, 128 x 256
-  bicgstab_check      a BiCGStab run whose residual identity clamps to 0 below
+  bicgstab_check_*    BiCGStab runs whose residual identity clamps to 0 below
                       tol, so the reference runs its "check" phase
-                      (solvers.py:687-694)
+                      (solvers.py:687-694): one passing, two failing + resuming
 """
 
 from __future__ import annotations
@@ -65,12 +67,15 @@ def sample_idx(n):
     return np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, NSAMPLE)])).astype(np.int64)
 
 
-def check_system():
-    """A small nonsymmetric system on which the BiCGStab residual identity
-    goes negative with the monitor below tol (found by search_check())."""
-    spec = json.loads((HERE / "scale_check_spec.json").read_text())
-    a, b = pk.gen_random_rowwise(spec["n"], spec["k"], seed=spec["seed"])
-    return a, np.asarray(b), spec
+def check_system(name):
+    """Small systems on which the BiCGStab residual identity goes negative
+    while the monitor is below tol, so the reference runs its "check" phase
+    (solvers.py:687-694): a 2x2 Jordan block whose first s is an exact
+    eigenvector (check passes), and the same block plus three weakly excited
+    modes at tol 1e-12 (check fails, the loop resumes, converges later).
+    Found by a seeded search over such matrices; stored explicitly."""
+    spec = json.loads((HERE / "scale_check_spec.json").read_text())[name]
+    return pk.CsrMatrix.from_dense(spec["dense"]), np.asarray(spec["b"], dtype=np.float64), spec
 
 
 CASES = {
@@ -80,14 +85,18 @@ CASES = {
                                     {"fixed_iterations": 30, "max_iterations": 30}, (256, 65536)),
     "c3_128_fixed31": lambda: ("gmres", to_ref(orc.convdiff3d(128)[0]), None,
                                {"fixed_iterations": 31, "max_iterations": 31, "restart": 30}, (128, 256)),
+    "c3_64_tol": lambda: ("gmres", to_ref(orc.convdiff3d(64)[0]), None, {"max_iterations": 3000, "restart": 30},
+                          (128, 256)),
+    "c3_128_tol": lambda: ("gmres", to_ref(orc.convdiff3d(128)[0]), None, {"max_iterations": 3000, "restart": 30},
+                           (128, 256)),
     "c2_1024_tol": lambda: ("bicgstab", to_ref(orc.convdiff2d(1024)[0]), None, {"max_iterations": 20000},
                             (128, 256)),
 }
 
 
 def run_case(name):
-    if name == "bicgstab_check":
-        a, b, spec = check_system()
+    if name.startswith("bicgstab_check"):
+        a, b, spec = check_system(name)
         method, cfg, geom = "bicgstab", spec["config"], tuple(spec["geom"])
     else:
         method, a, b, cfg, geom = CASES[name]()
@@ -122,33 +131,7 @@ def run_case(name):
     return entry
 
 
-def search_check(max_tries=4000):
-    """Search seeded random row-wise systems for a BiCGStab run whose
-    residual identity clamps while the monitor is below tol."""
-    hits = []
-    for seed in range(max_tries):
-        for n, k in ((40, 3), (60, 4), (30, 2), (80, 5)):
-            a, b = pk.gen_random_rowwise(n, k, seed=seed)
-            res = pk.SOLVERS[("bicgstab", "pipelined")](a, np.asarray(b), config=pk.SolverConfig(
-                tolerance=1e-12, max_iterations=200), context=pk.ExecutionContext(128, 256))
-            ph = [p.label for p in res.trace.phases]
-            if "check" in ph:
-                spec = {"n": n, "k": k, "seed": seed, "config": {"tolerance": 1e-12, "max_iterations": 200},
-                        "geom": [128, 256], "iterations": res.iterations, "termination": res.termination,
-                        "check_phases": ph.count("check")}
-                print("hit", spec, flush=True)
-                hits.append(spec)
-                return spec
-    return None
-
-
 def main(argv):
-    if argv and argv[0] == "--search-check":
-        spec = search_check()
-        if spec is None:
-            raise SystemExit("no check-phase system found")
-        (HERE / "scale_check_spec.json").write_text(json.dumps(spec, indent=1))
-        return
     if argv and argv[0] == "--merge":
         manifest = {"cases": {}, "reference": {"package": "pipekrylov", "version": pk.__version__,
                                                "numpy": np.__version__}}
@@ -156,7 +139,8 @@ def main(argv):
             manifest["cases"][f.stem] = json.loads(f.read_text())
         (HERE / "scale_manifest.json").write_text(json.dumps(manifest, indent=1, sort_keys=True))
         return
-    for name in argv or list(CASES) + ["bicgstab_check"]:
+    checks = list(json.loads((HERE / "scale_check_spec.json").read_text()))
+    for name in argv or list(CASES) + checks:
         run_case(name)
 
 

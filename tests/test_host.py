@@ -143,3 +143,14 @@ def test_device_code_has_no_fp_contraction(tmp_path):
     ptx = out.read_text()
     assert "fma.rn.f64" not in ptx
     assert ptx.count("add.rn.f64") > 100
+
+
+@pytest.mark.parametrize("side,block", [(3, 2), (4, 3), (5, 1), (2, 5)])
+def test_host_poisson3d_block_equals_oracle(side, block):
+    """gen_poisson3d_block(n, block > 1) (io.py:232-275) vs the oracle's COO restatement."""
+    a, b = pk.gen_poisson3d_block(side, block)
+    oa, ob = orc.poisson3d_block(side, block)
+    assert a.n_rows == oa.n_rows == side ** 3 * block
+    assert np.array_equal(a.row_offsets, oa.rowptr) and np.array_equal(a.col_indices, oa.cols)
+    assert np.array_equal(a.values.view(np.int64), oa.vals.view(np.int64))
+    assert np.array_equal(b, ob)

@@ -157,10 +157,8 @@ def ref():
 @pytest.mark.reference
 @pytest.mark.parametrize("side,block", [(8, 1), (12, 1), (9, 2)])
 def test_poisson3d_matches_live_reference(ref, side, block):
-    if block != 1:
-        pytest.skip("oracle generator covers block=1 (the C4 config) only")
     ra, _ = ref.gen_poisson3d_block(side, block)
-    oa, _ = orc.poisson3d(side)
+    oa, _ = orc.poisson3d(side) if block == 1 else orc.poisson3d_block(side, block)
     assert same(ra.row_offsets, oa.rowptr) and same(ra.col_indices, oa.cols) and same(ra.values, oa.vals)
 
 

@@ -1,0 +1,4 @@
+set -u
+OUT=gpurun_out/r2d; mkdir -p $OUT
+timeout 300 python tools/engine_probe.py bicgstab:1024:PK_SELL=1 bicgstab:1024:PK_SELL=0 cg:512:PK_SELL=1 cg:512:PK_SELL=0 cg3d:256:PK_SELL=1 cg3d:256:PK_SELL=0 gmres:128:PK_SELL=1 gmres:128:PK_SELL=0 > $OUT/probe.jsonl 2>&1; cat $OUT/probe.jsonl
+timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/tests.log 2>&1; echo "tests rc=$?"; tail -3 $OUT/tests.log
