@@ -414,3 +414,18 @@ def test_sell32_unstructured_rows_equal_csr(pk, n, k, method):
     assert same(r_csr.x, r_sell.x) and same(r_csr.residual_history, r_sell.residual_history)
     dm.set_format("csr", ctx)
     assert dm.format == "csr"
+
+
+@pytest.mark.parametrize("m", [34, 40, 70])
+def test_gmres_restart_longer_than_one_update_chunk(pk, m):
+    """GMRES(m) with m - 1 > 32 basis vectors per update: the Gram-Schmidt
+    accumulation runs in 32-vector chunks through an accumulator vector
+    (OpGsAcc, then OpGsUpdate) -- the same rounding sequence as the
+    reference's single accumulated sum (fused.py:268-272)."""
+    a, b = pk.convdiff2d(24)
+    cfg = pk.SolverConfig(restart=m, max_iterations=200)
+    res = pk.gmres_pipelined(a, b, config=cfg)
+    assert_identical(res, oracle_run("gmres", a, b, (128, 256), restart=m, max_iterations=200))
+    cfgf = pk.SolverConfig(restart=m, fixed_iterations=m + 3, max_iterations=m + 3)
+    resf = pk.gmres_pipelined(a, b, config=cfgf, context=pk.ExecutionContext(8, 32))
+    assert_identical(resf, oracle_run("gmres", a, b, (8, 32), restart=m, fixed=m + 3, max_iterations=m + 3))

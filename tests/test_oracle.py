@@ -196,3 +196,18 @@ def test_classical_match_live_reference(ref, method, geom):
         assert same(np.asarray(oo["history"]), np.asarray(rr.residual_history))
         assert same(oo["x"], rr.x)
         assert oo["true_final_residual"] == rr.true_final_residual
+
+
+@pytest.mark.reference
+@pytest.mark.parametrize("m", [34, 40, 70])
+def test_gmres_long_restart_oracle_matches_live_reference(ref, m):
+    """The oracle the GPU's GMRES(m > 33) is checked against, vs the live
+    reference on the same conv-diff system (any restart length)."""
+    a = orc.convdiff2d(24)[0]
+    ra = ref.CsrMatrix(a.n_rows, a.n_cols, a.rowptr, a.cols, a.vals)
+    b = np.ones(a.n_rows)
+    rr = ref.SOLVERS[("gmres", "pipelined")](ra, b, config=ref.SolverConfig(restart=m, max_iterations=200))
+    oo = orc.SOLVERS["gmres"](a, b, restart=m, max_iterations=200, geom=(128, 256))
+    assert oo["iterations"] == rr.iterations and oo["termination"] == rr.termination
+    assert same(np.asarray(oo["history"]), np.asarray(rr.residual_history))
+    assert same(oo["x"], rr.x)
