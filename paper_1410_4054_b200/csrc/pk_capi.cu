@@ -98,6 +98,7 @@ struct pk_ctx {
   void* ws_cache = nullptr;       // cached solver workspaces (pk_solvers.inc WsCache)
   void (*ws_cache_free)(pk_ctx*) = nullptr;
   bool ws_cache_on = true;        // PK_WS_CACHE=0 disables the workspace / graph cache
+  int gs_chunk = 16;              // PK_GS_CHUNK: basis vectors per Gram-Schmidt update pass (4..32; 16 measured best, GMRES(30) 128^3)
   pk_debug_fn dbg = nullptr;      // per-iteration diagnostics hook (pk_ctx_set_debug)
   void* dbg_user = nullptr;
   bool pdl = false;               // PK_PDL=1: programmatic stream serialization (measured slower, off)
@@ -315,9 +316,12 @@ __global__ void __launch_bounds__(kThreads, 4)
     const int g = (int)(lid0 / geo.gs);
     if (tid == 0) {
       const unsigned per = (unsigned)(geo.gs / LPB);
-      unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
+      unsigned tk = ticket_add(scr.gtick + g, 1u);
       int last = (tk == per - 1);
-      if (last) scr.gtick[g] = 0u;
+      if (last) {
+        scr.gtick[g] = 0u;
+        acquire_fence();
+      }
       s_flag = last;
     }
     __syncthreads();
@@ -336,9 +340,10 @@ __global__ void __launch_bounds__(kThreads, 4)
     __syncthreads();
     if (tid == 0) {
       unsigned* ticket = st ? &st->ticket : scr.ticket;
-      unsigned tk = atomic_add_acq_rel(ticket, (unsigned)ncomplete);
+      unsigned tk = ticket_add(ticket, (unsigned)ncomplete);
       if (tk + (unsigned)ncomplete == (unsigned)geo.n_groups) {
         *ticket = 0u;
+        acquire_fence();
         s_last = 1;
       }
     }
@@ -936,21 +941,28 @@ static int gs_acc_t(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* 
   return launch_sweep(c, s, n, op, ScalarPtrs{}, st, gate);
 }
 
-// Gram-Schmidt update over nb basis vectors: chunks of kGsChunk accumulate
-// through `acc` (an n-vector; needed only when nb > kGsChunk), the last chunk
-// subtracts the sum from v and emits the <v,v> partials.
-constexpr int kGsChunk = 32;
+// Gram-Schmidt update over nb basis vectors: chunks of gs_chunk (<= 32)
+// vectors accumulate through `acc` (an n-vector; needed only when nb >
+// gs_chunk), the last chunk subtracts the sum from v and emits the <v,v>
+// partials.  Same rounding sequence for any chunking.
+constexpr int kGsChunk = 32;  // largest chunk (the accumulator is allocated for restart - 1 > gs_chunk)
 
 static int gs_update_any(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
                          const double* coef_dev, double* part, SolveState* st = nullptr, int gate = GATE_NONE,
                          int fin = FIN_NONE, int fin_arg = 0, double* acc = nullptr) {
   int j0 = 0;
   const double* acc_in = nullptr;
-  while (nb - j0 > kGsChunk) {
+  const int ch = acc ? c->gs_chunk : kGsChunk;
+  while (nb - j0 > ch) {
     if (!acc) return fail(PK_ERR_INVALID, "Gram-Schmidt update over more than 32 vectors needs an accumulator");
-    PK_TRY(gs_acc_t<kGsChunk>(c, s, n, kGsChunk, basis + j0, coef_dev + j0, acc_in, acc, st, gate));
+    int rc;
+    if (ch <= 4) rc = gs_acc_t<4>(c, s, n, ch, basis + j0, coef_dev + j0, acc_in, acc, st, gate);
+    else if (ch <= 8) rc = gs_acc_t<8>(c, s, n, ch, basis + j0, coef_dev + j0, acc_in, acc, st, gate);
+    else if (ch <= 16) rc = gs_acc_t<16>(c, s, n, ch, basis + j0, coef_dev + j0, acc_in, acc, st, gate);
+    else rc = gs_acc_t<32>(c, s, n, ch, basis + j0, coef_dev + j0, acc_in, acc, st, gate);
+    PK_TRY(rc);
     acc_in = acc;
-    j0 += kGsChunk;
+    j0 += ch;
   }
   const int r = nb - j0;
   const double* const* bb = basis + j0;
@@ -1016,6 +1028,7 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e8 = getenv("PK_SELL")) c->sell_default = atoi(e8) != 0;
   if (const char* e9 = getenv("PK_STAGE")) c->staged = atoi(e9) != 0;
   if (const char* e10 = getenv("PK_WS_CACHE")) c->ws_cache_on = atoi(e10) != 0;
+  if (const char* e11 = getenv("PK_GS_CHUNK")) c->gs_chunk = std::max(4, std::min(32, atoi(e11)));
   // keep freed workspace memory in the stream-ordered pool between solves
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -1717,7 +1730,7 @@ extern "C" int pk_gs_update(pk_ctx* c, int64_t n, double* v, int32_t nb, const d
     PK_CUDA(cudaGetLastError());
   }
   double* acc = nullptr;
-  if (nb > kGsChunk) PK_CUDA(cudaMallocAsync(&acc, (size_t)std::max<int64_t>(n, 1) * 8, c->stream));
+  if (nb > c->gs_chunk) PK_CUDA(cudaMallocAsync(&acc, (size_t)std::max<int64_t>(n, 1) * 8, c->stream));
   int rc = gs_update_any(c, c->stream, n, v, nb, basis, coeffs, norm_partials, nullptr, GATE_NONE, FIN_NONE, 0, acc);
   if (acc) cudaFreeAsync(acc, c->stream);
   return rc;

@@ -325,18 +325,20 @@ __device__ __forceinline__ void group_tree(const Geom& geo, int g, const double*
 // the engine
 // ---------------------------------------------------------------------------
 
-// Ticket increment with acquire-release semantics at gpu scope: the release
-// half publishes this CTA's spill/partials before the ticket moves, the
-// acquire half makes every other CTA's published data visible to the CTA
-// that draws the last ticket (it then reads them with L2 loads,
-// ld.global.cg).  No __threadfence(): that would also emit an L1
-// invalidation (CCTL.IVALL) and throw away the L1-resident CSR lines of every
-// warp on the SM.
-__device__ __forceinline__ unsigned atomic_add_acq_rel(unsigned* p, unsigned v) {
+// Ticket increment with release semantics at gpu scope (MEMBAR + ATOM): it
+// publishes this CTA's spill / partials before the ticket moves.  The CTA
+// that draws the LAST ticket then executes acquire_fence() before it reads
+// the others' data (with L2 loads, ld.global.cg) -- only there, because the
+// acquire half emits an L1 invalidation (CCTL.IVALL) that would otherwise
+// throw away the L1-resident CSR lines of every warp on the SM at every
+// ticket.  Other threads of that CTA (warp) read after a barrier (shuffle)
+// that orders them behind the fencing thread.
+__device__ __forceinline__ unsigned ticket_add(unsigned* p, unsigned v) {
   unsigned r;
-  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
   return r;
 }
+__device__ __forceinline__ void acquire_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // Scalar binary-counter leaf push for quantity q (stk laid out as LeafStack).
 template <int NQ>
@@ -437,9 +439,12 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         const int g = (int)(lid0 / geo.gs);
         if (tid == 0) {
           const unsigned per = (unsigned)(geo.gs / 32);
-          unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
+          unsigned tk = ticket_add(scr.gtick + g, 1u);
           int last = (tk == per - 1);
-          if (last) scr.gtick[g] = 0u;
+          if (last) {
+            scr.gtick[g] = 0u;
+            acquire_fence();
+          }
           s_flag = last;
         }
         __syncthreads();
@@ -516,9 +521,12 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
         }
         __syncthreads();
         if (tid == 0) {
-          unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
+          unsigned tk = ticket_add(scr.gtick + g, 1u);
           int lastp = (tk == (unsigned)F - 1);
-          if (lastp) scr.gtick[g] = 0u;
+          if (lastp) {
+            scr.gtick[g] = 0u;
+            acquire_fence();
+          }
           s_flag = lastp;
         }
         __syncthreads();
@@ -560,9 +568,10 @@ __device__ __forceinline__ bool engine_run(const Geom& geo, const Op& op, double
     if (ncomplete > 0) {
       __syncthreads();
       if (tid == 0) {
-        unsigned tk = atomic_add_acq_rel(ticket, (unsigned)ncomplete);
+        unsigned tk = ticket_add(ticket, (unsigned)ncomplete);
         if (tk + (unsigned)ncomplete == (unsigned)geo.n_groups) {
           *ticket = 0u;
+          acquire_fence();
           s_last = 1;
         }
       }
@@ -738,18 +747,22 @@ __device__ __forceinline__ bool engine_chain_staged(const Geom& geo, const Op& o
       const int g = (int)(lid0 / geo.gs);
       if (tid == 0) {
         const unsigned per = (unsigned)(geo.gs / 32);
-        unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
+        unsigned tk = ticket_add(scr.gtick + g, 1u);
         int last = (tk == per - 1);
-        if (last) scr.gtick[g] = 0u;
+        if (last) {
+          scr.gtick[g] = 0u;
+          acquire_fence();
+        }
         s_flag = last;
       }
       __syncthreads();
       if (s_flag) {
         group_tree<NQ>(geo, g, scr.spill, tail, part, ld, col0, nstore);
         if (tid == 0) {
-          unsigned tk = atomic_add_acq_rel(ticket, 1u);
+          unsigned tk = ticket_add(ticket, 1u);
           if (tk + 1u == (unsigned)geo.n_groups) {
             *ticket = 0u;
+            acquire_fence();
             s_last = 1;
           }
         }
@@ -939,18 +952,22 @@ __device__ __forceinline__ bool engine_warp_chain(const Geom& geo, const Op& op,
     int lastg = 0;
     if (lane == 0) {
       const unsigned per = (unsigned)(geo.gs / 32);
-      unsigned tk = atomic_add_acq_rel(scr.gtick + g, 1u);
+      unsigned tk = ticket_add(scr.gtick + g, 1u);
       lastg = (tk == per - 1);
-      if (lastg) scr.gtick[g] = 0u;
+      if (lastg) {
+        scr.gtick[g] = 0u;
+        acquire_fence();
+      }
     }
     lastg = __shfl_sync(kFull, lastg, 0);
     if (lastg) {
       group_tree_warp<NQ>(geo, g, scr.spill, stk, part, ld, col0, nstore);
       int l = 0;
       if (lane == 0) {
-        unsigned tk = atomic_add_acq_rel(ticket, 1u);
+        unsigned tk = ticket_add(ticket, 1u);
         if (tk + 1u == (unsigned)geo.n_groups) {
           *ticket = 0u;
+          acquire_fence();
           l = 1;
         }
       }
