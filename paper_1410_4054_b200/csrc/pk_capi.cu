@@ -98,6 +98,7 @@ struct pk_ctx {
   void* ws_cache = nullptr;       // cached solver workspaces (pk_solvers.inc WsCache)
   void (*ws_cache_free)(pk_ctx*) = nullptr;
   bool ws_cache_on = true;        // PK_WS_CACHE=0 disables the workspace / graph cache
+  bool lane_engine = true;        // PK_LANE=0: elementwise reductions on the CTA engine instead of engine_lane
   int gs_chunk = 16;              // PK_GS_CHUNK: basis vectors per Gram-Schmidt update pass (4..32; 16 measured best, GMRES(30) 128^3)
   pk_debug_fn dbg = nullptr;      // per-iteration diagnostics hook (pk_ctx_set_debug)
   void* dbg_user = nullptr;
@@ -110,7 +111,9 @@ struct pk_ctx {
   bool sweep_one_batch = false;   // PK_SWEEP_ONEBATCH: elementwise sweeps with one V-row batch per thread
   bool staged = true;             // PK_STAGE=0: off (only in -DPK_STAGED_ENGINE builds: the cp.async-staged
                                   // CHAIN engine, measured slower; compiling it in also slows the default engine)
-  bool sell_default = false;      // PK_SELL=1: new matrices also get a SELL-32 copy the kernels walk (measured slower on B200 for the stencil configs; off)
+  int sell_mode = 2;              // PK_SELL: 0 never / 1 always / 2 auto -- new matrices get a SELL-32 copy the kernels
+                                  // walk when n >= 2^19 and nnz >= 12 n (measured: random 16/row, n = 1M: CG 344 -> 260
+                                  // us/iter; stencils (5-7/row) and short matrices gain nothing or lose)
   bool sweep_scalar = false;      // PK_SWEEP_SCALAR=1: scalar grid-stride sweeps instead of the 16-byte k_sweep2
   bool warp_k1 = true;            // PK_WARP_K1: n <= G systems on the warp chain engine (vs LEAF)        // PK_MAT_DISCARD=0: keep consumed lines in L2 (write-back on eviction)
 };
@@ -190,6 +193,31 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const Geom g2 = geo;
     finalize(st, fin, fin_arg, ing, smem, (int)(engine_smem_bytes(g2, NQ, U) / sizeof(double)));
   }
+}
+
+#ifndef PK_LANE_D_WIDE
+#define PK_LANE_D_WIDE 4
+#endif
+
+// LANE engine kernel (elementwise operators on CHAIN geometries): one thread
+// per reduction lane, D chunks of loads in flight (pk_reduce.cuh engine_lane).
+template <int NQ, int D, class Op>
+__global__ void __launch_bounds__(kLaneThreads)
+    k_reduce_lane(const __grid_constant__ Geom geo, const __grid_constant__ Op op0, ScalarPtrs sp, double* part,
+                  int ld, int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin,
+                  int fin_arg, int smem_d) {
+  extern __shared__ double smem[];
+  pdl_wait();
+  pdl_trigger();
+  if (skip && *(volatile const int32_t*)skip) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  const GateVals gv = gate_load(st, gate);
+  Op op = op0;
+  op.scalars(sp);
+  if (!gate_eval(st, gate, ing, gv)) return;
+  const bool last = engine_lane<NQ, D>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+  if (last && fin != FIN_NONE && st && threadIdx.x < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
 }
 
 constexpr int kWarpStage2Doubles = 1024;  // stage-2 staging of the warp engine's finalizer
@@ -690,6 +718,21 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
       return PK_OK;
     }
   }
+  if constexpr (!Op::kSpmv) {
+    if (c->lane_engine && !geo.leaf && geo.gs >= 32 && geo.K >= 2) {
+      // elementwise operator on a CHAIN geometry: thread = lane, in-register
+      // chain fold, no staging (engine_lane)
+      constexpr int D = NQ >= 8 ? PK_LANE_D_WIDE : 4;  // chunks of loads in flight per thread
+      const int T = lane_cta_threads(geo);
+      const int sd = (int)std::max<size_t>(std::max<size_t>(engine_tail_doubles(geo, NQ), (size_t)NQ * T), 1024);
+      auto kl = k_reduce_lane<NQ, D, Op>;
+      PK_TRY(allow_dynamic_smem(kl, (size_t)sd * sizeof(double)));
+      cudaError_t e = launch_k(c->pdl, kl, dim3((unsigned)((geo.G + T - 1) / T)), dim3(T), (size_t)sd * sizeof(double),
+                               s, geo, op, sp, part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin, fin_arg, sd);
+      if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("lane engine launch: ") + cudaGetErrorString(e));
+      return PK_OK;
+    }
+  }
   if constexpr (NQ <= 4) {
   // single-chunk lanes (n <= G) also go to the warp engine when the context
   // allows it (PK_WARP_K1): one warp per 32 lanes, no leaf stacks or splits
@@ -1025,9 +1068,10 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e5 = getenv("PK_WARP_K1")) c->warp_k1 = atoi(e5) != 0;
   if (const char* e6 = getenv("PK_SWEEP_ONEBATCH")) c->sweep_one_batch = atoi(e6) != 0;
   if (const char* e7 = getenv("PK_SWEEP_SCALAR")) c->sweep_scalar = atoi(e7) != 0;
-  if (const char* e8 = getenv("PK_SELL")) c->sell_default = atoi(e8) != 0;
+  if (const char* e8 = getenv("PK_SELL")) c->sell_mode = atoi(e8);
   if (const char* e9 = getenv("PK_STAGE")) c->staged = atoi(e9) != 0;
   if (const char* e10 = getenv("PK_WS_CACHE")) c->ws_cache_on = atoi(e10) != 0;
+  if (const char* e12 = getenv("PK_LANE")) c->lane_engine = atoi(e12) != 0;
   if (const char* e11 = getenv("PK_GS_CHUNK")) c->gs_chunk = std::max(4, std::min(32, atoi(e11)));
   // keep freed workspace memory in the stream-ordered pool between solves
   cudaMemPool_t pool;
@@ -1458,7 +1502,9 @@ extern "C" int pk_mat_get_format(const pk_mat* m, int32_t* format, int64_t* stor
 
 // the context's default format for new matrices (PK_SELL env, see pk_ctx)
 static int apply_default_format(pk_ctx* c, pk_mat* m) {
-  return c->sell_default ? pk_mat_set_format(c, m, PK_FMT_SELL32) : PK_OK;
+  const bool want = c->sell_mode == 1 ||
+                    (c->sell_mode == 2 && m->n_rows >= (int64_t(1) << 19) && m->nnz >= 12 * m->n_rows && !m->row64);
+  return want ? pk_mat_set_format(c, m, PK_FMT_SELL32) : PK_OK;
 }
 
 extern "C" int pk_mat_destroy(pk_mat* m) {

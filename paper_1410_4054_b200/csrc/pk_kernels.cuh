@@ -1021,6 +1021,7 @@ struct OpGsUpdate {
   const double* b[NB];
   const double* coef;    // device [nb], finalized by the previous kernel
   const double* acc_in;  // running sum of the earlier chunks, or null (start from 0.0)
+  double cf[NB];         // the coefficients, loaded once per thread in scalars()
   struct Item { double v, a; double b[NB]; };
   __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.v = v[i];
@@ -1035,13 +1036,15 @@ struct OpGsUpdate {
   __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&cc)[M]) const {
     double acc = it.a;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(__ldg(coef + j), it.b[j]));
+    for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(cf[j], it.b[j]));
     double vn = (nb > 0 || acc_in) ? sub_rn(it.v, acc) : it.v;
     v[i] = vn;
     cc[0] = mul_rn(vn, vn);
   }
   __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
     if (sp.a) coef = sp.a;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) cf[j] = j < nb ? __ldg(coef + j) : 0.0;
   }
 };
 
@@ -1056,6 +1059,7 @@ struct OpGsAcc {
   const double* coef;
   const double* acc_in;
   double* acc_out;
+  double cf[NB];
   struct Item { double a; double b[NB]; };
   __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.a = acc_in ? __ldg(acc_in + i) : 0.0;
@@ -1069,10 +1073,13 @@ struct OpGsAcc {
   __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&)[M]) const {
     double acc = it.a;
 #pragma unroll
-    for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(__ldg(coef + j), it.b[j]));
+    for (int j = 0; j < NB; ++j) if (j < nb) acc = add_rn(acc, mul_rn(cf[j], it.b[j]));
     acc_out[i] = acc;
   }
-  __device__ __forceinline__ void scalars(const ScalarPtrs&) {}
+  __device__ __forceinline__ void scalars(const ScalarPtrs&) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) cf[j] = j < nb ? __ldg(coef + j) : 0.0;
+  }
 };
 
 // fused_gs_normalize (fused.py:280-305): v *= inv; <r, v>.

@@ -977,6 +977,110 @@ __device__ __forceinline__ bool engine_warp_chain(const Geom& geo, const Op& op,
   return last;
 }
 
+// ---------------------------------------------------------------------------
+// LANE engine: elementwise operators (no SpMV) on CHAIN geometries (K >= 2)
+// ---------------------------------------------------------------------------
+//
+// One thread per reduction lane t of [0, G): the thread walks its own chain
+// rows t, t + G, t + 2G, ... (each warp's 32 rows of a chunk are consecutive
+// lanes: coalesced) and folds the contributions in registers in chunk order
+// -- exactly linalg.py:300-303 -- with the loads of D chunks issued before
+// their folds.  Elementwise rows have no dependent loads, so nothing needs
+// staging: no shared-memory fold, no per-batch barrier.  A CTA of T = min(gs,
+// kLaneThreads) lanes evaluates the group's halving tree itself when it holds
+// the whole group (T == gs); otherwise lane values go to the spill buffer and
+// the CTA completing the group runs group_tree().  Global ticket + finalizer as
+// in engine_run().
+constexpr int kLaneThreads = 256;
+
+__host__ __device__ inline int lane_cta_threads(const Geom& g) { return g.gs < kLaneThreads ? g.gs : kLaneThreads; }
+
+template <int NQ, int D, class Op>
+__device__ __forceinline__ bool engine_lane(const Geom& geo, const Op& op, double* smem, double* part, int ld,
+                                            int col0, int nstore, const Scratch& scr, unsigned* ticket) {
+  __shared__ int s_flag;
+  __shared__ int s_last;
+  const int T = blockDim.x;
+  const int tid = threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * T + tid;  // lane id
+  const bool lane_ok = t < geo.G;
+  if (tid == 0) s_last = 0;
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  if (lane_ok) {
+    for (int64_t k0 = 0; k0 < geo.K; k0 += D) {
+      typename Op::Item it[D];
+      int64_t row[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        row[d] = (k0 + d) * geo.G + t;
+        const int64_t rc = row[d] < geo.n ? row[d] : t;  // clamped: every load unconditional
+        op.load((uint32_t)rc, it[d]);
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        if (k0 + d < geo.K && row[d] < geo.n) {
+          double c[NQ];
+          op.compute((uint32_t)row[d], it[d], c);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) acc[q] = add_rn(acc[q], c[q]);
+        }
+      }
+    }
+  }
+  const int g = (int)((int64_t)blockIdx.x * T / geo.gs);
+  if (T == geo.gs) {
+    // the CTA holds the whole group: its halving tree (linalg.py:304-307) here
+    block_tree<NQ>(acc, smem, T);
+    if (tid == 0 && part) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < nstore) part[(int64_t)g * ld + col0 + q] = acc[q];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned tk = ticket_add(ticket, 1u);
+      if (tk + 1u == (unsigned)geo.n_groups) {
+        *ticket = 0u;
+        acquire_fence();
+        s_last = 1;
+      }
+    }
+  } else {
+    if (lane_ok) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < nstore) scr.spill[(int64_t)q * geo.G + t] = acc[q];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned per = (unsigned)(geo.gs / T);
+      unsigned tk = ticket_add(scr.gtick + g, 1u);
+      int last = (tk == per - 1);
+      if (last) {
+        scr.gtick[g] = 0u;
+        acquire_fence();
+      }
+      s_flag = last;
+    }
+    __syncthreads();
+    if (s_flag) {
+      group_tree<NQ>(geo, g, scr.spill, smem, part, ld, col0, nstore);
+      if (tid == 0) {
+        unsigned tk = ticket_add(ticket, 1u);
+        if (tk + 1u == (unsigned)geo.n_groups) {
+          *ticket = 0u;
+          acquire_fence();
+          s_last = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
 // Grid-stride thread-per-row sweep (no reduction): plain SpMV / updates.
 template <class Op>
 __device__ __forceinline__ void sweep_rows(int64_t n, const Op& op) {

@@ -18,3 +18,15 @@ def test_bench_spawns_ranks_without_torchrun():
     lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
     assert sorted(l["rank"] for l in lines) == [0, 1]
     assert all(l["world"] == 2 for l in lines)
+
+
+def test_lpt_assignment_balances_the_batch():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    sides = [128, 256, 512]
+    costs = [5 * sides[i % 3] ** 3 * 3.0 for i in range(4096)]
+    for world in (1, 2, 4, 8):
+        owner = bench.lpt_assign(costs, world)
+        loads = [sum(c for c, o in zip(costs, owner) if o == r) for r in range(world)]
+        assert max(loads) <= (sum(costs) / world) * 1.01
