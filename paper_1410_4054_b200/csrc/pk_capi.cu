@@ -98,6 +98,10 @@ struct pk_ctx {
   void* ws_cache = nullptr;       // cached solver workspaces (pk_solvers.inc WsCache)
   void (*ws_cache_free)(pk_ctx*) = nullptr;
   bool ws_cache_on = true;        // PK_WS_CACHE=0 disables the workspace / graph cache
+  bool lane_spmv = true;          // PK_LANE_SPMV=0: SpMV operators on the CTA / warp CHAIN engines instead
+  int lane_spmv_maxk = 8;         // PK_LANE_SPMV_MAXK: longest lane chain (K) sent to the pipelined lane engine
+                                  // (measured: CG 512^2, K = 8: 19.2 -> 17.7 us/iter; K = 32 (C2): 83 -> 101, so
+                                  // long chains stay on the CTA engine)
   bool lane_engine = true;        // PK_LANE=0: elementwise reductions on the CTA engine instead of engine_lane
   int gs_chunk = 16;              // PK_GS_CHUNK: basis vectors per Gram-Schmidt update pass (4..32; 16 measured best, GMRES(30) 128^3)
   pk_debug_fn dbg = nullptr;      // per-iteration diagnostics hook (pk_ctx_set_debug)
@@ -217,6 +221,31 @@ __global__ void __launch_bounds__(kLaneThreads)
   op.scalars(sp);
   if (!gate_eval(st, gate, ing, gv)) return;
   const bool last = engine_lane<NQ, D>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+  if (last && fin != FIN_NONE && st && threadIdx.x < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
+}
+
+#ifndef PK_LANE_P
+#define PK_LANE_P 2
+#endif
+
+// Software-pipelined LANE engine for SpMV operators (engine_lane_spmv).
+template <int NQ, int P, class Op>
+__global__ void __launch_bounds__(kLaneThreads, 1)
+    k_reduce_lane_spmv(const __grid_constant__ Geom geo, const __grid_constant__ Op op0, ScalarPtrs sp, double* part,
+                       int ld, int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip,
+                       int fin, int fin_arg, int smem_d) {
+  extern __shared__ double smem[];
+  pdl_wait();
+  pdl_trigger();
+  if (skip && *(volatile const int32_t*)skip) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  const GateVals gv = gate_load(st, gate);
+  Op op = op0;
+  op.scalars(sp);
+  if (!gate_eval(st, gate, ing, gv)) return;
+  const bool last =
+      engine_lane_spmv<NQ, P>(geo, op, smem, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
   if (last && fin != FIN_NONE && st && threadIdx.x < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
 }
 
@@ -733,6 +762,18 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
       return PK_OK;
     }
   }
+  if constexpr (Op::kSpmv && NQ <= 4) {
+    if (c->lane_spmv && !geo.leaf && geo.gs >= 32 && geo.K >= 2 && geo.K <= c->lane_spmv_maxk) {
+      const int T = lane_cta_threads(geo);
+      const int sd = (int)std::max<size_t>(std::max<size_t>(engine_tail_doubles(geo, NQ), (size_t)NQ * T), 1024);
+      auto kl = k_reduce_lane_spmv<NQ, PK_LANE_P, Op>;
+      PK_TRY(allow_dynamic_smem(kl, (size_t)sd * sizeof(double)));
+      cudaError_t e = launch_k(c->pdl, kl, dim3((unsigned)((geo.G + T - 1) / T)), dim3(T), (size_t)sd * sizeof(double),
+                               s, geo, op, sp, part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin, fin_arg, sd);
+      if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("lane SpMV engine launch: ") + cudaGetErrorString(e));
+      return PK_OK;
+    }
+  }
   if constexpr (NQ <= 4) {
   // single-chunk lanes (n <= G) also go to the warp engine when the context
   // allows it (PK_WARP_K1): one warp per 32 lanes, no leaf stacks or splits
@@ -1072,6 +1113,8 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e9 = getenv("PK_STAGE")) c->staged = atoi(e9) != 0;
   if (const char* e10 = getenv("PK_WS_CACHE")) c->ws_cache_on = atoi(e10) != 0;
   if (const char* e12 = getenv("PK_LANE")) c->lane_engine = atoi(e12) != 0;
+  if (const char* e13 = getenv("PK_LANE_SPMV")) c->lane_spmv = atoi(e13) != 0;
+  if (const char* e14 = getenv("PK_LANE_SPMV_MAXK")) c->lane_spmv_maxk = atoi(e14);
   if (const char* e11 = getenv("PK_GS_CHUNK")) c->gs_chunk = std::max(4, std::min(32, atoi(e11)));
   // keep freed workspace memory in the stream-ordered pool between solves
   cudaMemPool_t pool;

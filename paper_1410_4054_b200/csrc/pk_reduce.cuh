@@ -1081,6 +1081,169 @@ __device__ __forceinline__ bool engine_lane(const Geom& geo, const Op& op, doubl
   return s_last != 0;
 }
 
+// ---------------------------------------------------------------------------
+// LANE engine for SpMV operators: a software-pipelined lane chain
+// ---------------------------------------------------------------------------
+//
+// Thread = reduction lane t, walking its chain rows kG + t (k = 0..K-1; a
+// warp's 32 rows of a chunk are consecutive: coalesced) and folding the
+// contributions in registers in chunk order.  A row's loads form a dependent
+// chain (row bounds -> columns/values -> gathered inputs), so the chain is
+// software-pipelined three deep: in every round the thread
+//   (1) folds the P chunks whose gathers were issued in the previous round,
+//   (2) issues the gathers of the P chunks whose columns arrived,
+//   (3) issues the column/value/own-vector loads of the P chunks whose bounds
+//       arrived, and
+//   (4) issues the row-bound loads of P new chunks,
+// so 3P chunks are in flight per thread and a round waits for ONE memory
+// latency instead of three, with no shared-memory fold and no barrier.  Rows
+// longer than kSlots finish their remaining entries at fold time.  A CTA of
+// T = min(gs, 256) lanes runs the group tree itself when it holds the whole
+// group; otherwise spill + group ticket as in engine_lane().
+template <int NQ, int P, class Op>
+__device__ __forceinline__ bool engine_lane_spmv(const Geom& geo, const Op& op, double* smem, double* part, int ld,
+                                                 int col0, int nstore, const Scratch& scr, unsigned* ticket) {
+  using RowT = typename Op::RowT;
+  constexpr int S = Op::kSlots;
+  constexpr bool sell = std::decay_t<decltype(op.A)>::kSell;
+  const RowT st = sell ? 32 : 1;
+  const int32_t* __restrict__ ci = sell ? op.A.sc : op.A.ci;
+  const double* __restrict__ va = sell ? op.A.sv : op.A.va;
+  __shared__ int s_flag;
+  __shared__ int s_last;
+  const int T = blockDim.x;
+  const int tid = threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * T + tid;
+  const bool lane_ok = t < geo.G;
+  if (tid == 0) s_last = 0;
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  // stage A: row bounds; B: columns, values, own-row item; C: gathered inputs
+  RowT aB[P], aE[P], bB[P], bE[P], cB[P], cE[P];
+  int32_t bC[P][S], cC[P][S];
+  double bV[P][S], cV[P][S];
+  typename Op::Item bI[P], cI[P];
+  typename Op::Gat cG[P][S];
+  int64_t aR[P], bR[P], cR[P];  // rows (-1: no row)
+#pragma unroll
+  for (int p = 0; p < P; ++p) { aR[p] = bR[p] = cR[p] = -1; }
+  const int64_t R = lane_ok ? (geo.K + P - 1) / P : 0;
+  for (int64_t r = 0; r < R + 3; ++r) {
+    // (1) fold stage C (chunks of round r - 3), in chunk order
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (cR[p] >= 0) {
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+          if (cB[p] + j * st < cE[p] && cC[p][j] >= 0) a = add_rn(a, mul_rn(cV[p][j], op.gval(cG[p][j])));
+        for (RowT k = cB[p] + S * st; k < cE[p]; k += st) {  // rows longer than kSlots
+          const int32_t cj = __ldg(ci + k);
+          if (cj < 0) continue;
+          typename Op::Gat g;
+          op.gload((uint32_t)cj, g);
+          a = add_rn(a, mul_rn(__ldg(va + k), op.gval(g)));
+        }
+        double c[NQ];
+        op.compute((uint32_t)cR[p], cI[p], a, c);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = add_rn(acc[q], c[q]);
+      }
+    }
+    // (2) stage B -> C: gathers
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      cR[p] = bR[p];
+      cB[p] = bB[p];
+      cE[p] = bE[p];
+      cI[p] = bI[p];
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        cC[p][j] = bC[p][j];
+        cV[p][j] = bV[p][j];
+        if (cR[p] >= 0) op.gload((uint32_t)(cC[p][j] < 0 ? 0 : cC[p][j]), cG[p][j]);
+      }
+    }
+    // (3) stage A -> B: columns, values, own-row loads
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      bR[p] = aR[p];
+      bB[p] = aB[p];
+      bE[p] = aE[p];
+      if (bR[p] >= 0) {
+        op.load((uint32_t)bR[p], bI[p]);
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          const RowT k = (bB[p] + j * st < bE[p]) ? bB[p] + j * st : bB[p];
+          const bool live = bE[p] > bB[p];
+          bC[p][j] = live ? __ldg(ci + k) : -1;
+          bV[p][j] = live ? __ldg(va + k) : 0.0;
+        }
+      }
+    }
+    // (4) new chunks -> stage A: row bounds
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int64_t k = r * P + p;
+      const int64_t row = k * geo.G + t;
+      aR[p] = (r < R && k < geo.K && row < geo.n) ? row : -1;
+      aB[p] = 1;
+      aE[p] = 0;
+      if (aR[p] >= 0) row_span(op.A, (uint32_t)row, aB[p], aE[p]);
+    }
+  }
+  const int g = (int)((int64_t)blockIdx.x * T / geo.gs);
+  if (T == geo.gs) {
+    block_tree<NQ>(acc, smem, T);
+    if (tid == 0 && part) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < nstore) part[(int64_t)g * ld + col0 + q] = acc[q];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned tk = ticket_add(ticket, 1u);
+      if (tk + 1u == (unsigned)geo.n_groups) {
+        *ticket = 0u;
+        acquire_fence();
+        s_last = 1;
+      }
+    }
+  } else {
+    if (lane_ok) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < nstore) scr.spill[(int64_t)q * geo.G + t] = acc[q];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned per = (unsigned)(geo.gs / T);
+      unsigned tk = ticket_add(scr.gtick + g, 1u);
+      int last = (tk == per - 1);
+      if (last) {
+        scr.gtick[g] = 0u;
+        acquire_fence();
+      }
+      s_flag = last;
+    }
+    __syncthreads();
+    if (s_flag) {
+      group_tree<NQ>(geo, g, scr.spill, smem, part, ld, col0, nstore);
+      if (tid == 0) {
+        unsigned tk = ticket_add(ticket, 1u);
+        if (tk + 1u == (unsigned)geo.n_groups) {
+          *ticket = 0u;
+          acquire_fence();
+          s_last = 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
 // Grid-stride thread-per-row sweep (no reduction): plain SpMV / updates.
 template <class Op>
 __device__ __forceinline__ void sweep_rows(int64_t n, const Op& op) {
