@@ -102,6 +102,8 @@ struct pk_ctx {
   int lane_spmv_maxk = 8;         // PK_LANE_SPMV_MAXK: longest lane chain (K) sent to the pipelined lane engine
                                   // (measured: CG 512^2, K = 8: 19.2 -> 17.7 us/iter; K = 32 (C2): 83 -> 101, so
                                   // long chains stay on the CTA engine)
+  bool gs_split = false;          // PK_GS_SPLIT=1: 16-byte update sweep + LANE-engine dot instead of the fused update
+                                  // (measured GMRES(30) 128^3: 219 vs 214 us/iter fused; off)
   bool lane_engine = true;        // PK_LANE=0: elementwise reductions on the CTA engine instead of engine_lane
   int gs_chunk = 16;              // PK_GS_CHUNK: basis vectors per Gram-Schmidt update pass (4..32; 16 measured best, GMRES(30) 128^3)
   pk_debug_fn dbg = nullptr;      // per-iteration diagnostics hook (pk_ctx_set_debug)
@@ -751,7 +753,11 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
     if (c->lane_engine && !geo.leaf && geo.gs >= 32 && geo.K >= 2) {
       // elementwise operator on a CHAIN geometry: thread = lane, in-register
       // chain fold, no staging (engine_lane)
-      constexpr int D = NQ >= 8 ? PK_LANE_D_WIDE : 4;  // chunks of loads in flight per thread
+      // chunks of loads in flight per thread, by the bytes a row loads: light
+      // rows (dots, normalize, updates) need many chunks to cover a latency,
+      // wide ones (multi-dot, Gram-Schmidt) few (registers)
+      constexpr size_t IB = sizeof(typename Op::Item);
+      constexpr int D = IB <= 32 ? 16 : (IB <= 64 ? 8 : (IB <= 160 ? PK_LANE_D_WIDE : 2));
       const int T = lane_cta_threads(geo);
       const int sd = (int)std::max<size_t>(std::max<size_t>(engine_tail_doubles(geo, NQ), (size_t)NQ * T), 1024);
       auto kl = k_reduce_lane<NQ, D, Op>;
@@ -824,6 +830,11 @@ struct HasVec2 : std::false_type {};
 template <class Op>
 struct HasVec2<Op, std::void_t<typename Op::Item2>> : std::true_type {};
 
+template <class Op, class = void>
+struct SweepPairs { static constexpr int value = 0; };
+template <class Op>
+struct SweepPairs<Op, std::void_t<decltype(Op::kPairs)>> { static constexpr int value = Op::kPairs; };
+
 #ifndef PK_SWEEP_PAIRS
 #define PK_SWEEP_PAIRS 4
 #endif
@@ -834,10 +845,10 @@ static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Scal
                         SolveState* st = nullptr, int gate = GATE_NONE) {
   if constexpr (HasVec2<Op>::value) {
     if (!c->sweep_scalar && op.aligned16()) {
+      constexpr int UP = SweepPairs<Op>::value > 0 ? SweepPairs<Op>::value : kSweepPairs;
       const int64_t np = n >> 1;
-      const int64_t grid = std::max<int64_t>(1, (np + 256 * kSweepPairs - 1) / (256 * kSweepPairs));
-      PK_CUDA(launch_k(c->pdl, k_sweep2<Op, kSweepPairs>, dim3((unsigned)grid), dim3(256), 0, s, n, op, sp, st,
-                       gate));
+      const int64_t grid = std::max<int64_t>(1, (np + 256 * UP - 1) / (256 * UP));
+      PK_CUDA(launch_k(c->pdl, k_sweep2<Op, UP>, dim3((unsigned)grid), dim3(256), 0, s, n, op, sp, st, gate));
       return PK_OK;
     }
   }
@@ -1025,6 +1036,24 @@ static int gs_acc_t(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* 
   return launch_sweep(c, s, n, op, ScalarPtrs{}, st, gate);
 }
 
+template <int NB>
+static int gs_sweep_t(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb, const double* const* basis,
+                      const double* coef_dev, const double* acc_in, SolveState* st, int gate) {
+  OpGsSweep<NB> op{};
+  op.v = v;
+  op.nb = nb;
+  op.coef = coef_dev;
+  op.acc_in = acc_in;
+  for (int j = 0; j < NB; ++j) op.b[j] = j < nb ? basis[j] : nullptr;
+  return launch_sweep(c, s, n, op, ScalarPtrs{coef_dev, nullptr, nullptr, nullptr}, st, gate);
+}
+
+// the lane / CTA CHAIN engines apply (K >= 2): the split update's dot runs on
+// the LANE engine; one-element-per-lane geometries keep the fused update
+static bool geo_is_leaf(const pk_ctx* c, int64_t n) {
+  return make_geom(n, c->ng, c->gs, min_units(c)).leaf != 0;
+}
+
 // Gram-Schmidt update over nb basis vectors: chunks of gs_chunk (<= 32)
 // vectors accumulate through `acc` (an n-vector; needed only when nb >
 // gs_chunk), the last chunk subtracts the sum from v and emits the <v,v>
@@ -1051,6 +1080,17 @@ static int gs_update_any(pk_ctx* c, cudaStream_t s, int64_t n, double* v, int nb
   const int r = nb - j0;
   const double* const* bb = basis + j0;
   const double* cd = coef_dev + j0;
+  if (c->gs_split && !geo_is_leaf(c, n)) {
+    // elementwise update through 16-byte accesses, then the <v,v> partials
+    int rc;
+    if (r <= 2) rc = gs_sweep_t<2>(c, s, n, v, r, bb, cd, acc_in, st, gate);
+    else if (r <= 4) rc = gs_sweep_t<4>(c, s, n, v, r, bb, cd, acc_in, st, gate);
+    else if (r <= 8) rc = gs_sweep_t<8>(c, s, n, v, r, bb, cd, acc_in, st, gate);
+    else if (r <= 16) rc = gs_sweep_t<16>(c, s, n, v, r, bb, cd, acc_in, st, gate);
+    else rc = gs_sweep_t<32>(c, s, n, v, r, bb, cd, acc_in, st, gate);
+    PK_TRY(rc);
+    return dot_partials(c, s, n, v, v, part, st, gate, fin, fin_arg);
+  }
   if (r <= 1) return gs_update_t<1>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
   if (r <= 2) return gs_update_t<2>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
   if (r <= 4) return gs_update_t<4>(c, s, n, v, r, bb, cd, acc_in, part, st, gate, fin, fin_arg);
@@ -1113,6 +1153,7 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e9 = getenv("PK_STAGE")) c->staged = atoi(e9) != 0;
   if (const char* e10 = getenv("PK_WS_CACHE")) c->ws_cache_on = atoi(e10) != 0;
   if (const char* e12 = getenv("PK_LANE")) c->lane_engine = atoi(e12) != 0;
+  if (const char* e15 = getenv("PK_GS_SPLIT")) c->gs_split = atoi(e15) != 0;
   if (const char* e13 = getenv("PK_LANE_SPMV")) c->lane_spmv = atoi(e13) != 0;
   if (const char* e14 = getenv("PK_LANE_SPMV_MAXK")) c->lane_spmv_maxk = atoi(e14);
   if (const char* e11 = getenv("PK_GS_CHUNK")) c->gs_chunk = std::max(4, std::min(32, atoi(e11)));

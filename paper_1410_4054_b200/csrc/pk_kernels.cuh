@@ -35,6 +35,9 @@
 #define PK_FIN_PREFETCH 0
 #endif
 
+#ifndef PK_BICG_U
+#define PK_BICG_U 2  // rows per thread per batch of the BiCGStab SpMV operators (engine batch = 8 U chunks)
+#endif
 #ifndef PK_BICGB_MINB
 #define PK_BICGB_MINB 4
 #endif
@@ -354,16 +357,41 @@ __device__ inline void finalize(SolveState* st, int fin, int arg, bool ing, doub
       break;
     }
     case FIN_GM_COEF: {
-      // arg = step index i (>= 2): columns 0..i-2 of p_coef
-      for (int j0 = 0; j0 < arg - 1; j0 += 4) {
-        const int nj = (arg - 1 - j0) < 4 ? (arg - 1 - j0) : 4;
-        const S2Col cs[4] = {{st->p_coef, st->m, j0}, {st->p_coef, st->m, j0 + (nj > 1)},
-                             {st->p_coef, st->m, j0 + 2 * (nj > 2)}, {st->p_coef, st->m, j0 + 3 * (nj > 3)}};
-        stage2_warp<4>(cs, ng, tot, buf, buf_d);
-        if (th < nj) {
-          st->coef[j0 + th] = tot[th];
-          st->R[(int64_t)(j0 + th) * st->m + (arg - 1)] = tot[th];
+      // arg = step index i (>= 2): columns 0..i-2 of p_coef, up to 32 at a
+      // time (lane c sums column j0 + c over the groups, serially, in group
+      // order -- linalg.py:311-320); the [ng][m] partials are staged through
+      // shared memory with coalesced loads
+      const int nc = arg - 1, m = st->m;
+      for (int j0 = 0; j0 < nc; j0 += 32) {
+        const int nj = (nc - j0) < 32 ? (nc - j0) : 32;
+        const int CH = buf_d / nj;
+        double t = 0.0;
+        for (int g0 = 0; g0 < ng; g0 += CH) {
+          const int cnt = (ng - g0) < CH ? (ng - g0) : CH;
+          __syncwarp();
+          for (int idx = th; idx < cnt * nj; idx += 32) {
+            const int g = idx / nj, c = idx - g * nj;
+            buf[c * CH + g] = __ldcg(st->p_coef + (int64_t)(g0 + g) * m + j0 + c);
+          }
+          __syncwarp();
+          if (th < nj) {
+            const double* b = buf + th * CH;
+            int g = 0;
+            for (; g + 8 <= cnt; g += 8) {
+              double v[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v[u] = b[g + u];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) t = add_rn(t, v[u]);
+            }
+            for (; g < cnt; ++g) t = add_rn(t, b[g]);
+          }
         }
+        if (th < nj) {
+          st->coef[j0 + th] = t;
+          st->R[(int64_t)(j0 + th) * m + (arg - 1)] = t;
+        }
+        __syncwarp();
       }
       break;
     }
@@ -645,7 +673,7 @@ struct OpBicgB {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
   static constexpr int kMinBlocks = PK_BICGB_MINB;
-  static constexpr int kRowsPerThread = 2;
+  static constexpr int kRowsPerThread = PK_BICG_U;
   static constexpr int kSlots = S_;
   Csr<RowT, SELL_> A;
   const double* r[2];
@@ -804,8 +832,8 @@ template <typename RowT_, int S_, bool SELL_ = false>
 struct OpBicgApNext {
   using RowT = RowT_;
   static constexpr bool kSpmv = true;
-  static constexpr int kMinBlocks = 4;
-  static constexpr int kRowsPerThread = 2;
+  static constexpr int kMinBlocks = PK_BICGB_MINB;
+  static constexpr int kRowsPerThread = PK_BICG_U;
   static constexpr int kSlots = S_;
   Csr<RowT, SELL_> A;
   double* r[2];
@@ -1060,7 +1088,29 @@ struct OpGsAcc {
   const double* acc_in;
   double* acc_out;
   double cf[NB];
+  static constexpr int kPairs = NB > 8 ? 1 : 2;
   struct Item { double a; double b[NB]; };
+  struct Item2 { double2 a; double2 b[NB]; };
+  __device__ __forceinline__ void load2(uint32_t i, Item2& t) const {
+    t.a = acc_in ? ld2(acc_in + i) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) t.b[j] = j < nb ? ld2(b[j] + i) : make_double2(0.0, 0.0);
+  }
+  __device__ __forceinline__ void compute2(uint32_t i, Item2& t) const {
+    double a0 = t.a.x, a1 = t.a.y;
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j < nb) {
+        a0 = add_rn(a0, mul_rn(cf[j], t.b[j].x));
+        a1 = add_rn(a1, mul_rn(cf[j], t.b[j].y));
+      }
+    st2(acc_out + i, a0, a1);
+  }
+  bool aligned16() const {
+    bool ok = al16(acc_out) && (!acc_in || al16(acc_in));
+    for (int j = 0; j < NB; ++j) ok = ok && (j >= nb || al16(b[j]));
+    return ok;
+  }
   __device__ __forceinline__ void load(uint32_t i, Item& it) const {
     it.a = acc_in ? __ldg(acc_in + i) : 0.0;
 #pragma unroll
@@ -1079,6 +1129,61 @@ struct OpGsAcc {
   __device__ __forceinline__ void scalars(const ScalarPtrs&) {
 #pragma unroll
     for (int j = 0; j < NB; ++j) cf[j] = j < nb ? __ldg(coef + j) : 0.0;
+  }
+};
+
+// Split Gram-Schmidt update, elementwise half (PK_GS_SPLIT): the same
+// v_new = v - acc (acc = acc_in + sum_j c_j b_j in basis order) as OpGsUpdate,
+// written through 16-byte accesses at full occupancy; the <v_new, v_new>
+// partials follow in a separate dot (OpDot on the LANE engine) -- the same
+// products in the same order, so the same bits, for one more read of v.
+template <int NB>
+struct OpGsSweep {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = 2;
+  static constexpr int kPairs = NB > 8 ? 1 : 2;
+  double* v;
+  int32_t nb;
+  const double* b[NB];
+  const double* coef;
+  const double* acc_in;
+  double cf[NB];
+  struct Item { double v, a; double b[NB]; };
+  struct Item2 { double2 v, a; double2 b[NB]; };
+  __device__ __forceinline__ void load(uint32_t i, Item& it) const {
+    it.v = v[i];
+    it.a = acc_in ? __ldg(acc_in + i) : 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) it.b[j] = j < nb ? __ldg(b[j] + i) : 0.0;
+  }
+  __device__ __forceinline__ double upd(double vv, double a, const double (&bb)[NB]) const {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) if (j < nb) a = add_rn(a, mul_rn(cf[j], bb[j]));
+    return (nb > 0 || acc_in) ? sub_rn(vv, a) : vv;
+  }
+  template <int M>
+  __device__ __forceinline__ void compute(uint32_t i, Item& it, double (&)[M]) const { v[i] = upd(it.v, it.a, it.b); }
+  __device__ __forceinline__ void load2(uint32_t i, Item2& t) const {
+    t.v = *reinterpret_cast<const double2*>(v + i);
+    t.a = acc_in ? ld2(acc_in + i) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) t.b[j] = j < nb ? ld2(b[j] + i) : make_double2(0.0, 0.0);
+  }
+  __device__ __forceinline__ void compute2(uint32_t i, Item2& t) const {
+    double b0[NB], b1[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) { b0[j] = t.b[j].x; b1[j] = t.b[j].y; }
+    st2(v + i, upd(t.v.x, t.a.x, b0), upd(t.v.y, t.a.y, b1));
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) {
+    if (sp.a) coef = sp.a;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) cf[j] = j < nb ? __ldg(coef + j) : 0.0;
+  }
+  bool aligned16() const {
+    bool ok = al16(v) && (!acc_in || al16(acc_in));
+    for (int j = 0; j < NB; ++j) ok = ok && (j >= nb || al16(b[j]));
+    return ok;
   }
 };
 

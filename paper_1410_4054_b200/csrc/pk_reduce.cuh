@@ -215,10 +215,10 @@ __device__ __forceinline__ void row_contrib(const Op& op, uint32_t row, double (
         val[j] = __ldg(va + k);
       }
 #pragma unroll
-      for (int j = 0; j < S; ++j) op.gload((uint32_t)(col[j] < 0 ? 0 : col[j]), gv[j]);
+      for (int j = 0; j < S; ++j) op.gload((uint32_t)(sell && col[j] < 0 ? 0 : col[j]), gv[j]);
 #pragma unroll
       for (int j = 0; j < S; ++j)
-        if (k0 + j * st < e && col[j] >= 0) acc = add_rn(acc, mul_rn(val[j], op.gval(gv[j])));
+        if (k0 + j * st < e && (!sell || col[j] >= 0)) acc = add_rn(acc, mul_rn(val[j], op.gval(gv[j])));
     }
     op.compute(row, it, acc, c);
   } else {
@@ -633,10 +633,10 @@ __device__ __forceinline__ void row_contrib_staged(const Op& op, uint32_t row, d
       val[j] = __ldg(va + k);
     }
 #pragma unroll
-    for (int j = 0; j < S; ++j) op.gload((uint32_t)(col[j] < 0 ? 0 : col[j]), gv[j]);
+    for (int j = 0; j < S; ++j) op.gload((uint32_t)(sell && col[j] < 0 ? 0 : col[j]), gv[j]);
 #pragma unroll
     for (int j = 0; j < S; ++j)
-      if (k0 + j * st < e && col[j] >= 0) acc = add_rn(acc, mul_rn(val[j], op.gval(gv[j])));
+      if (k0 + j * st < e && (!sell || col[j] >= 0)) acc = add_rn(acc, mul_rn(val[j], op.gval(gv[j])));
   }
   op.compute(row, it, acc, c);
 }
@@ -885,17 +885,17 @@ __device__ __forceinline__ void rows_contrib(const Op& op, const Geom& geo, int6
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int j = 0; j < S; ++j) op.gload((uint32_t)(col[r][j] < 0 ? 0 : col[r][j]), gv[r][j]);
+      for (int j = 0; j < S; ++j) op.gload((uint32_t)(sell && col[r][j] < 0 ? 0 : col[r][j]), gv[r][j]);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       double acc = 0.0;
 #pragma unroll
       for (int j = 0; j < S; ++j)
-        if (b[r] + j * st < e[r] && col[r][j] >= 0) acc = add_rn(acc, mul_rn(val[r][j], op.gval(gv[r][j])));
+        if (b[r] + j * st < e[r] && (!sell || col[r][j] >= 0)) acc = add_rn(acc, mul_rn(val[r][j], op.gval(gv[r][j])));
       // rows longer than S: the rest in order, straight from memory
       for (RowT k = b[r] + S * st; k < e[r]; k += st) {
         const int32_t cj = __ldg(ci + k);
-        if (cj < 0) continue;
+        if (sell && cj < 0) continue;
         typename Op::Gat g;
         op.gload((uint32_t)cj, g);
         acc = add_rn(acc, mul_rn(__ldg(va + k), op.gval(g)));
@@ -1137,10 +1137,10 @@ __device__ __forceinline__ bool engine_lane_spmv(const Geom& geo, const Op& op, 
         double a = 0.0;
 #pragma unroll
         for (int j = 0; j < S; ++j)
-          if (cB[p] + j * st < cE[p] && cC[p][j] >= 0) a = add_rn(a, mul_rn(cV[p][j], op.gval(cG[p][j])));
+          if (cB[p] + j * st < cE[p] && (!sell || cC[p][j] >= 0)) a = add_rn(a, mul_rn(cV[p][j], op.gval(cG[p][j])));
         for (RowT k = cB[p] + S * st; k < cE[p]; k += st) {  // rows longer than kSlots
           const int32_t cj = __ldg(ci + k);
-          if (cj < 0) continue;
+          if (sell && cj < 0) continue;
           typename Op::Gat g;
           op.gload((uint32_t)cj, g);
           a = add_rn(a, mul_rn(__ldg(va + k), op.gval(g)));
@@ -1162,7 +1162,7 @@ __device__ __forceinline__ bool engine_lane_spmv(const Geom& geo, const Op& op, 
       for (int j = 0; j < S; ++j) {
         cC[p][j] = bC[p][j];
         cV[p][j] = bV[p][j];
-        if (cR[p] >= 0) op.gload((uint32_t)(cC[p][j] < 0 ? 0 : cC[p][j]), cG[p][j]);
+        if (cR[p] >= 0) op.gload((uint32_t)(sell && cC[p][j] < 0 ? 0 : cC[p][j]), cG[p][j]);
       }
     }
     // (3) stage A -> B: columns, values, own-row loads
@@ -1177,7 +1177,7 @@ __device__ __forceinline__ bool engine_lane_spmv(const Geom& geo, const Op& op, 
         for (int j = 0; j < S; ++j) {
           const RowT k = (bB[p] + j * st < bE[p]) ? bB[p] + j * st : bB[p];
           const bool live = bE[p] > bB[p];
-          bC[p][j] = live ? __ldg(ci + k) : -1;
+          bC[p][j] = live ? __ldg(ci + k) : 0;  // an empty row gathers a valid column and adds nothing
           bV[p][j] = live ? __ldg(va + k) : 0.0;
         }
       }

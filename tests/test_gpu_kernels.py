@@ -225,3 +225,26 @@ def test_vec_update_kinds_bitwise():
             got = yd.cpu().numpy()
             assert np.array_equal(got.view(np.int64)[~np.isnan(ref)], ref.view(np.int64)[~np.isnan(ref)]), kind
             assert np.array_equal(np.isnan(got), np.isnan(ref)), kind
+
+
+@pytest.mark.parametrize("geom", [(16, 64), (4, 256), (1, 1024), (8, 32), (2, 4096)])
+def test_spmv_fused_empty_and_long_rows(pk, fused, geom):
+    """Rows with no entries and rows longer than the kernels' slot count (the
+    remainder path), on short lane chains (2 <= K <= 8: the pipelined lane
+    engine) and others; CSR and SELL-32 walks vs the oracle, bitwise."""
+    rng = np.random.default_rng(3)
+    n = 5000
+    lens = rng.integers(0, 12, n)
+    lens[rng.random(n) < 0.1] = 0
+    lens[::97] = 40
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens])
+    vals = rng.standard_normal(rows.size)
+    a = pk.CsrMatrix.from_coo(n, n, rows, cols, vals)
+    p, w = rng.standard_normal(n), rng.standard_normal(n)
+    ctx = pk.ExecutionContext(*geom)
+    oq, opart = orc.spmv_fused(a, p, ("input", "result", w), geom)
+    for fmt in ("csr", "sell32"):
+        dm = pk.DeviceMatrix.upload(pk.context_for(ctx), a).set_format(fmt, ctx)
+        q, part = fused.spmv_fused(dm, dev(p), ("input", "result", dev(w)), ctx)
+        assert same(host(q), oq) and same(host(part), opart), fmt
