@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "pipekrylov_b200.h"
+#include "pk_bulk.cuh"
 #include "pk_kernels.cuh"
 #include "pk_reduce.cuh"
 #include "pk_state.cuh"
@@ -121,6 +122,11 @@ struct pk_ctx {
                                   // walk when n >= 2^19 and nnz >= 12 n (measured: random 16/row, n = 1M: CG 344 -> 260
                                   // us/iter; stencils (5-7/row) and short matrices gain nothing or lose)
   bool sweep_scalar = false;      // PK_SWEEP_SCALAR=1: scalar grid-stride sweeps instead of the 16-byte k_sweep2
+  int tile_mink = 0;              // PK_TILE_MINK: shortest lane chain (K) sent to the TILE engine (0 = off; experimental)
+  bool bulk = true;               // PK_BULK=0: SpMV operators on long lane chains use the CTA CHAIN engine instead of
+                                  // the TMA-fed BULK engine (pk_bulk.cuh)
+  int bulk_mink = 9;              // PK_BULK_MINK: shortest lane chain (K) sent to the BULK engine
+  int bulk_maxk = 32;             // PK_BULK_MAXK: longest (measured slower on GMRES 128^3 K = 64, CG 256^3 K = 512)
   bool warp_k1 = true;            // PK_WARP_K1: n <= G systems on the warp chain engine (vs LEAF)        // PK_MAT_DISCARD=0: keep consumed lines in L2 (write-back on eviction)
 };
 
@@ -128,6 +134,7 @@ struct pk_mat {
   uint64_t uid = 0;            // unique per matrix object (workspace-cache key)
   int device = 0;
   int64_t n_rows = 0, n_cols = 0, nnz = 0, max_row = 0;
+  int64_t blk_max = -1;        // most entries in an aligned 32-row block (BULK engine slots)
   bool row64 = false;
   void* rowptr = nullptr;
   int32_t* cols = nullptr;
@@ -252,6 +259,44 @@ __global__ void __launch_bounds__(kLaneThreads, 1)
 }
 
 constexpr int kWarpStage2Doubles = 1024;  // stage-2 staging of the warp engine's finalizer
+
+#ifndef PK_BULK_W
+#define PK_BULK_W 4
+#endif
+#ifndef PK_BULK_MINB
+#define PK_BULK_MINB 7
+#endif
+#ifndef PK_BULK_R
+#define PK_BULK_R 3  // data slots (chunks in flight) per row warp
+#endif
+
+#ifdef PK_BULK_TRACE
+extern "C" int pk_debug_bulk_trace(void* dev_buf) {
+  unsigned long long* p = (unsigned long long*)dev_buf;
+  return cudaMemcpyToSymbol(g_bulk_trace, &p, sizeof(p)) == cudaSuccess ? PK_OK : PK_ERR_CUDA;
+}
+#endif
+
+// BULK CHAIN engine (pk_bulk.cuh): one CTA per 32-lane unit, warp 0 = TMA
+// producer + ordered fold, warps 1..W = rows from shared memory.
+template <int NQ, int W, int R, int MINB, class Op>
+__global__ void __launch_bounds__(32 * (W + 1), MINB)
+    k_reduce_bulk(const __grid_constant__ Geom geo, const __grid_constant__ Op op0, ScalarPtrs sp, double* part,
+                  int ld, int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin,
+                  int fin_arg, const __grid_constant__ BulkCfg bc, int smem_d) {
+  extern __shared__ __align__(128) unsigned char bsm[];
+  pdl_wait();
+  pdl_trigger();
+  if (skip && *(volatile const int32_t*)skip) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  const GateVals gv = gate_load(st, gate);
+  Op op = op0;
+  op.scalars(sp);
+  if (!gate_eval(st, gate, ing, gv)) return;
+  const bool last = engine_bulk<NQ, W, R>(geo, op, bsm, bc, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
+  if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing, reinterpret_cast<double*>(bsm + bc.base), smem_d);
+}
 
 // One warp per CTA, one unit per warp (CHAIN mapping with group_size >= 32).
 template <int NQ, int R, class Op>
@@ -406,6 +451,153 @@ __global__ void __launch_bounds__(kThreads, 4)
         s_last = 1;
       }
     }
+  }
+  __syncthreads();
+  if (s_last && fin != FIN_NONE && st && tid < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
+}
+
+// ---------------------------------------------------------------------------
+// TILE engine: rows at streaming speed, each group folded by the CTA that
+// completes it (SpMV operators on CHAIN geometries, group_size % 256 == 0)
+// ---------------------------------------------------------------------------
+//
+// The work is cut into tiles of 256 consecutive rows: tile (g, k, s) = rows
+// k G + g gs + 256 s + [0, 256) -- the chunk-k rows of lanes [256 s, 256 s +
+// 256) of group g.  A persistent grid walks the tiles in GROUP-MAJOR order
+// (t = (g K + k) sub + s), one row per thread with the lean thread-per-row
+// code (row_contrib, the same arithmetic as every other engine), and stores
+// the NQ contributions to the contribution buffer cb[q][row].  After each
+// tile the CTA bumps the group's tile counter (release); the CTA completing
+// the group's K * sub-th tile (acquire) folds the group at once: thread l
+// sums lane l's chain cb[q][l], cb[q][l + G], ... in chunk order
+// (linalg.py:300-303; rows past n add +0.0 like in the fused engines), the
+// CTA runs the group's halving tree (linalg.py:304-307) and takes the global
+// ticket; the CTA completing the last group runs the finalizer.
+//
+// No CTA ever waits for another (no grid barrier: safe under concurrent
+// launches), rows run at full occupancy with no staging and no per-batch
+// barrier, and -- group-major -- a group's contributions are folded about
+// one wave after they were written, so they are read back from L2 and then
+// discarded there (discard.global.L2: no write-back).  Same operations, same
+// operands, same order as the fused engines: bit-identical partials.
+#ifndef PK_TILE_MINB
+#define PK_TILE_MINB 4
+#endif
+template <int NQ, class Op>
+__global__ void __launch_bounds__(256, PK_TILE_MINB)
+    k_reduce_tiles(const __grid_constant__ Geom geo, const __grid_constant__ Op op0, ScalarPtrs sp, double* part,
+                   int ld, int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin,
+                   int fin_arg, double* __restrict__ cb, int smem_d, int discard) {
+  extern __shared__ double smem[];
+  __shared__ int s_fold;
+  __shared__ int s_last;
+  pdl_wait();
+  pdl_trigger();
+  if (skip && *(volatile const int32_t*)skip) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  const GateVals gv = gate_load(st, gate);
+  Op op = op0;
+  op.scalars(sp);
+  if (!gate_eval(st, gate, ing, gv)) return;
+  const int tid = threadIdx.x;
+  const int64_t n = geo.n, G = geo.G, K = geo.K;
+  const int sub = geo.gs / 256;  // tiles per (group, chunk)
+  const int64_t per_g = K * sub;
+  const int64_t T = per_g * geo.n_groups;
+  unsigned* ticket = st ? &st->ticket : scr.ticket;
+  if (tid == 0) s_last = 0;
+  for (int64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const int g = (int)(t / per_g);
+    const int64_t rem = t - (int64_t)g * per_g;
+    const int64_t k = rem / sub;
+    const int s = (int)(rem - k * sub);
+    const int64_t row = k * G + (int64_t)g * geo.gs + 256 * s + tid;
+    if (row < n) {
+      double c[NQ];
+      row_contrib<NQ>(op, (uint32_t)row, c);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (q < nstore) cb[(int64_t)q * n + row] = c[q];
+    }
+    __syncthreads();
+    if (tid == 0) {
+#ifdef PK_TILE_RELAXED
+      const unsigned tk = atomicAdd(scr.gtick + g, 1u);  // experiment only: no release ordering
+#else
+      const unsigned tk = ticket_add(scr.gtick + g, 1u);
+#endif
+      const int f = tk == (unsigned)(per_g - 1);
+      if (f) {
+        scr.gtick[g] = 0u;
+        acquire_fence();
+      }
+      s_fold = f;
+    }
+    __syncthreads();
+    if (!s_fold) continue;
+    // ---- fold group g: lanes g gs + 256 j + tid, chunk order ----
+    double v[NQ];
+    for (int j = 0; j < sub; ++j) {
+      const int64_t lane = (int64_t)g * geo.gs + 256 * j + tid;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        double acc = 0.0;
+        if (q < nstore) {
+          const double* pq = cb + (int64_t)q * n + lane;
+          constexpr int UF = 16;
+          int64_t kk = 0;
+          for (; kk < K; kk += UF) {
+            double x[UF];
+#pragma unroll
+            for (int u = 0; u < UF; ++u) {
+              const int64_t r = (kk + u) * G + lane;
+              x[u] = (kk + u < K && r < n) ? __ldcg(pq + (kk + u) * G) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < UF; ++u)
+              if (kk + u < K) acc = add_rn(acc, x[u]);
+          }
+        }
+        v[q] = acc;
+        if (sub > 1 && q < nstore) scr.spill[(int64_t)q * G + lane] = acc;
+      }
+    }
+    if (discard) {
+      // the group's contribution lines are dead: drop them from L2 without a
+      // write-back (thread 16 i owns the 128-B line of lanes 16 i .. 16 i + 15)
+      __syncthreads();
+      if ((tid & 15) == 0) {
+        for (int j = 0; j < sub; ++j)
+          for (int q = 0; q < nstore; ++q)
+            for (int64_t kk = 0; kk < K; ++kk) {
+              const int64_t r = kk * G + (int64_t)g * geo.gs + 256 * j + tid;
+              if (r + 15 < n) asm volatile("discard.global.L2 [%0], 128;" ::"l"(cb + (int64_t)q * n + r) : "memory");
+            }
+      }
+    }
+    if (sub == 1) {
+      // the group's 256 lanes are this CTA's threads: halving tree directly
+      block_tree<NQ>(v, smem, 256);
+      if (tid == 0 && part) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          if (q < nstore) part[(int64_t)g * ld + col0 + q] = v[q];
+      }
+      __syncthreads();
+    } else {
+      __syncthreads();  // the spill was written by this CTA's threads
+      group_tree<NQ>(geo, g, scr.spill, smem, part, ld, col0, nstore);
+    }
+    if (tid == 0) {
+      const unsigned tk = ticket_add(ticket, 1u);
+      if (tk + 1u == (unsigned)geo.n_groups) {
+        *ticket = 0u;
+        acquire_fence();
+        s_last = 1;
+      }
+    }
+    __syncthreads();
   }
   __syncthreads();
   if (s_last && fin != FIN_NONE && st && tid < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
@@ -639,6 +831,11 @@ static bool mat_applies(const pk_ctx* c, const Geom& geo) {
   return c->mat_mink > 0 && !geo.leaf && geo.K >= c->mat_mink;
 }
 
+// TILE engine (k_reduce_tiles): CHAIN geometries with whole 256-lane tiles
+static bool tiles_apply(const pk_ctx* c, const Geom& geo) {
+  return c->tile_mink > 0 && !geo.leaf && geo.gs >= 256 && geo.gs % 256 == 0 && geo.K >= c->tile_mink;
+}
+
 // L2 discard of consumed contribution lines: only when every warp's 32-lane
 // segment is whole 128-B lines (n and G multiples of 32)
 static int mat_discard(const pk_ctx* c, const Geom& geo) {
@@ -647,7 +844,7 @@ static int mat_discard(const pk_ctx* c, const Geom& geo) {
 
 static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
   Geom geo = make_geom(n, c->ng, c->gs, min_units(c));
-  if (mat_applies(c, geo)) {
+  if (mat_applies(c, geo) || tiles_apply(c, geo)) {
     // SpMV operators carry at most 4 quantities
     const size_t mneed = (size_t)n * (size_t)std::min(std::max(nq, 1), 4);
     if (mneed > c->mat_cap) {
@@ -769,6 +966,40 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
     }
   }
   if constexpr (Op::kSpmv && NQ <= 4) {
+    if (tiles_apply(c, geo) && c->mat && c->mat_cap >= (size_t)n * (size_t)nstore) {
+      auto kt = k_reduce_tiles<NQ, Op>;
+      const size_t tail = geo.gs > 256 ? engine_tail_doubles(geo, NQ) : (size_t)NQ * 256;
+      const int sd = (int)std::max<size_t>(tail, 1024);
+      PK_TRY(allow_dynamic_smem(kt, (size_t)sd * sizeof(double)));
+      const int64_t tiles = geo.K * (geo.gs / 256) * geo.n_groups;
+      const int grid = engine_grid(c, kt, (size_t)sd * sizeof(double), tiles, 256);
+      cudaError_t e = launch_k(c->pdl, kt, dim3((unsigned)grid), dim3(256), (size_t)sd * sizeof(double), s, geo, op, sp,
+                               part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin, fin_arg, c->mat, sd,
+                               mat_discard(c, geo));
+      if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("tile engine launch: ") + cudaGetErrorString(e));
+      return PK_OK;
+    }
+  }
+  if constexpr (Op::kSpmv && NQ <= 4) {
+    if constexpr (!std::decay_t<decltype(op.A)>::kSell) {
+      if (c->bulk && !geo.leaf && geo.gs >= 32 && geo.K >= c->bulk_mink && geo.K <= c->bulk_maxk && op.A.blk >= 0) {
+        constexpr int W = PK_BULK_W, R = PK_BULK_R;
+        const BulkCfg bc = bulk_cfg<NQ, W, R, Op>(op.A.blk);
+        const size_t tail = std::max(warp_chain_smem_bytes(geo, NQ), (size_t)kWarpStage2Doubles * sizeof(double));
+        const size_t smem = std::max((size_t)bc.total, (size_t)bc.base + tail);
+        if (smem <= 100 * 1024 && op.A.maxr <= Op::kSlots) {
+          auto kb = k_reduce_bulk<NQ, W, R, PK_BULK_MINB, Op>;
+          PK_TRY(allow_dynamic_smem(kb, smem));
+          const int smem_d = (int)((smem - bc.base) / sizeof(double));
+          cudaError_t e = launch_k(c->pdl, kb, dim3((unsigned)geo.units), dim3(32 * (W + 1)), smem, s, geo, op, sp,
+                                   part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin, fin_arg, bc, smem_d);
+          if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("bulk engine launch: ") + cudaGetErrorString(e));
+          return PK_OK;
+        }
+      }
+    }
+  }
+  if constexpr (Op::kSpmv && NQ <= 4) {
     if (c->lane_spmv && !geo.leaf && geo.gs >= 32 && geo.K >= 2 && geo.K <= c->lane_spmv_maxk) {
       const int T = lane_cta_threads(geo);
       const int sd = (int)std::max<size_t>(std::max<size_t>(engine_tail_doubles(geo, NQ), (size_t)NQ * T), 1024);
@@ -865,6 +1096,8 @@ static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Scal
 template <typename RowT, bool SELL = false>
 static Csr<RowT, SELL> csr_of(const pk_mat* a) {
   Csr<RowT, SELL> A{(const RowT*)a->rowptr, a->cols, a->vals};
+  A.blk = (int32_t)std::min<int64_t>(a->blk_max, INT32_MAX);
+  A.maxr = (int32_t)std::min<int64_t>(a->max_row, INT32_MAX);
   if constexpr (SELL) {
     A.sp = (const RowT*)a->sell_ptr;
     A.sc = a->sell_cols;
@@ -1153,6 +1386,10 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e9 = getenv("PK_STAGE")) c->staged = atoi(e9) != 0;
   if (const char* e10 = getenv("PK_WS_CACHE")) c->ws_cache_on = atoi(e10) != 0;
   if (const char* e12 = getenv("PK_LANE")) c->lane_engine = atoi(e12) != 0;
+  if (const char* e19 = getenv("PK_TILE_MINK")) c->tile_mink = atoi(e19);
+  if (const char* e16 = getenv("PK_BULK")) c->bulk = atoi(e16) != 0;
+  if (const char* e20 = getenv("PK_BULK_MAXK")) c->bulk_maxk = atoi(e20);
+  if (const char* e17 = getenv("PK_BULK_MINK")) c->bulk_mink = std::max(2, atoi(e17));
   if (const char* e15 = getenv("PK_GS_SPLIT")) c->gs_split = atoi(e15) != 0;
   if (const char* e13 = getenv("PK_LANE_SPMV")) c->lane_spmv = atoi(e13) != 0;
   if (const char* e14 = getenv("PK_LANE_SPMV_MAXK")) c->lane_spmv_maxk = atoi(e14);
@@ -1585,7 +1822,46 @@ extern "C" int pk_mat_get_format(const pk_mat* m, int32_t* format, int64_t* stor
 }
 
 // the context's default format for new matrices (PK_SELL env, see pk_ctx)
+// most entries in an aligned 32-row block [32 b, 32 b + 32) -- a BULK engine
+// chunk (pk_bulk.cuh); atomicMax over the blocks
+template <typename RowT>
+__global__ void k_blk_max(int64_t n, const RowT* __restrict__ rp, unsigned long long* mx) {
+  const int64_t nb = (n + 31) / 32;
+  unsigned long long m = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = (b + 1) * 32 < n ? (b + 1) * 32 : n;
+    const unsigned long long d = (unsigned long long)(rp[e] - rp[b * 32]);
+    m = d > m ? d : m;
+  }
+  if (m) atomicMax(mx, m);
+}
+
+static int compute_blk_max(pk_ctx* c, pk_mat* m) {
+  if (m->n_rows == 0) {
+    m->blk_max = 0;
+    return PK_OK;
+  }
+  unsigned long long* d = nullptr;
+  PK_CUDA(cudaMalloc(&d, 8));
+  cudaError_t e = cudaMemsetAsync(d, 0, 8, c->stream);
+  const int64_t nb = (m->n_rows + 31) / 32;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nb + 255) / 256, (int64_t)c->sm_count * 8));
+  if (e == cudaSuccess) {
+    if (m->row64) k_blk_max<int64_t><<<g, 256, 0, c->stream>>>(m->n_rows, (const int64_t*)m->rowptr, d);
+    else k_blk_max<int32_t><<<g, 256, 0, c->stream>>>(m->n_rows, (const int32_t*)m->rowptr, d);
+    e = cudaGetLastError();
+  }
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("block scan: ") + cudaGetErrorString(e));
+  m->blk_max = (int64_t)h;
+  return PK_OK;
+}
+
 static int apply_default_format(pk_ctx* c, pk_mat* m) {
+  PK_TRY(compute_blk_max(c, m));
   const bool want = c->sell_mode == 1 ||
                     (c->sell_mode == 2 && m->n_rows >= (int64_t(1) << 19) && m->nnz >= 12 * m->n_rows && !m->row64);
   return want ? pk_mat_set_format(c, m, PK_FMT_SELL32) : PK_OK;

@@ -146,6 +146,8 @@ struct Csr {
   const RowT* sp = nullptr;   // SELL-32 slice offsets (entries), n_slices + 1
   const int32_t* sc = nullptr;
   const double* sv = nullptr;
+  int32_t blk = -1;           // host: most entries in an aligned 32-row block (BULK engine slot size), -1 unknown
+  int32_t maxr = 0;           // host: longest row
 };
 
 // [b, e) walk of a row and the slot stride: CSR (rp[row], rp[row + 1], 1) or
