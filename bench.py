@@ -279,8 +279,8 @@ def kernel_roofline(pk, dm, ctx, b, iters=200):
     _, res = solve_resident("bicgstab", dm, b, config=cfg, context=ctx, profile=True)
     ks, kl = res.diagnostics["kernel_seconds"], res.diagnostics["kernel_launches"]
     bc = b_csr(n, dm.nnz)
-    kernels = [("k_reduce<OpBicgB> (s-update + As = A s + 4 dots)", bc + 32 * n, ks[0], kl[0]),
-               ("k_reduce<OpBicgApNext> (Ap' = A p' + 2 dots)", bc + 32 * n, ks[1], kl[1]),
+    kernels = [("k_reduce<OpBicgB> (CTA CHAIN engine: s-update + As = A s + 4 dots)", bc + 32 * n, ks[0], kl[0]),
+               ("k_reduce_bulk<OpBicgApNext> (BULK engine, TMA-fed: Ap' = A p' + 2 dots)", bc + 32 * n, ks[1], kl[1]),
                ("k_sweep2<OpBicgXrpSweep> (xrp update, 16-byte accesses)", 64 * n, ks[2], kl[2])]
     peak, kind = peaks()
     rows = []

@@ -58,9 +58,18 @@ __device__ __forceinline__ void btrace(int slot) {
     g_bulk_trace[(size_t)blockIdx.x * 32 + slot] = t;
   }
 }
+__device__ __forceinline__ void btrace_abs(size_t slot) {
+  if (g_bulk_trace && (threadIdx.x & 31) == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_bulk_trace[slot] = t;
+  }
+}
 #define PK_BT(s) btrace(s)
+#define PK_BTA(s) btrace_abs(s)
 #else
 #define PK_BT(s)
+#define PK_BTA(s)
 #endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -109,6 +118,7 @@ struct BulkCfg {
   int32_t capc;  // column bytes per slot (>= the largest aligned range)
   int32_t capv;
   int32_t total; // bytes
+  int32_t pdl;   // launched with programmatic stream serialization
 };
 
 constexpr int kBulkCR = 1;  // contribution slots per row warp
@@ -140,10 +150,15 @@ __host__ inline BulkCfg bulk_cfg(int64_t blk_max) {
 // chunk j's rows out of the slot (rows of at most kSlots entries: a row's
 // columns / values fit in registers), i.e. before its gathers -- R - 1 chunks
 // of CSR are always in flight per warp.  Warp 0 only folds.
-template <int NQ, int W, int R, class Op>
-__device__ __forceinline__ bool engine_bulk(const Geom& geo, const Op& op, unsigned char* sm, const BulkCfg& bc,
+// `sync()` is called by every thread once the CTA's first R chunks per row
+// warp are in flight (their CSR bytes depend only on the matrix): it waits
+// for the previous kernel (programmatic dependent launch), loads the
+// operator's scalars and evaluates the gate; false = skip this launch (the
+// in-flight copies are drained first).
+template <int NQ, int W, int R, class Op, class Sync>
+__device__ __forceinline__ bool engine_bulk(const Geom& geo, Op& op, unsigned char* sm, const BulkCfg& bc,
                                             double* part, int ld, int col0, int nstore, const Scratch& scr,
-                                            unsigned* ticket) {
+                                            unsigned* ticket, Sync sync) {
   using RowT = typename Op::RowT;
   constexpr int S = Op::kSlots;
   constexpr int CR = kBulkCR;
@@ -165,6 +180,7 @@ __device__ __forceinline__ bool engine_bulk(const Geom& geo, const Op& op, unsig
   if (warp == 0) PK_BT(0);
 
   if (warp == 0) {
+    if (!sync()) return false;
     // ---------------- fold warp: the lane chains in chunk order ----------------
     double acc[NQ];
 #pragma unroll
@@ -273,6 +289,11 @@ __device__ __forceinline__ bool engine_bulk(const Geom& geo, const Op& op, unsig
   };
   for (int j = 0; j < nj && j < R; ++j) issue(j);
   if (wi == 0) PK_BT(4);
+  if (!sync()) {
+    // skipped launch: the issued copies still land in this CTA's shared memory
+    for (int j = 0; j < nj && j < R; ++j) mbar_wait(full + wi * R + j, 0u);
+    return false;
+  }
   typename Op::Item itn;
   uint32_t rown = 0;
   bool okn = false;

@@ -123,10 +123,19 @@ struct pk_ctx {
                                   // us/iter; stencils (5-7/row) and short matrices gain nothing or lose)
   bool sweep_scalar = false;      // PK_SWEEP_SCALAR=1: scalar grid-stride sweeps instead of the 16-byte k_sweep2
   int tile_mink = 0;              // PK_TILE_MINK: shortest lane chain (K) sent to the TILE engine (0 = off; experimental)
+  int vec_min_avg = 24;           // PK_VEC_MINAVG: matrices with >= this many entries per row on average take the VEC
+                                  // row-sum pre-pass (0 = off)
+  double* vecbuf = nullptr;       // its row sums, vec_cap doubles
+  size_t vec_cap = 0;
   bool bulk = true;               // PK_BULK=0: SpMV operators on long lane chains use the CTA CHAIN engine instead of
                                   // the TMA-fed BULK engine (pk_bulk.cuh)
+  bool bulk_pdl = false;          // PK_BULK_PDL=1: BULK kernels launch programmatically (their CSR prologue overlaps
+                                  // the previous kernel's tail; measured slower on C2: 94.5 vs 82.3 us/iter -- the
+                                  // waiting CTAs hold the registers / shared memory the previous kernel's last wave needs)
   int bulk_mink = 9;              // PK_BULK_MINK: shortest lane chain (K) sent to the BULK engine
   int bulk_maxk = 32;             // PK_BULK_MAXK: longest (measured slower on GMRES 128^3 K = 64, CG 256^3 K = 512)
+  int bulk_maxq = 2;              // PK_BULK_MAXQ: operators with at most this many dot quantities (C2: Ap' = A p' + 2
+                                  // dots 35.3-36.8 vs 37.3-38.0 us; As = A s + 4 dots 44.1-45.7 vs 42.7-43.8)
   bool warp_k1 = true;            // PK_WARP_K1: n <= G systems on the warp chain engine (vs LEAF)        // PK_MAT_DISCARD=0: keep consumed lines in L2 (write-back on eviction)
 };
 
@@ -135,6 +144,7 @@ struct pk_mat {
   int device = 0;
   int64_t n_rows = 0, n_cols = 0, nnz = 0, max_row = 0;
   int64_t blk_max = -1;        // most entries in an aligned 32-row block (BULK engine slots)
+  bool vec_rows = false;       // long rows: SpMV row sums by the VEC pre-pass (k_rowsum_warp)
   bool row64 = false;
   void* rowptr = nullptr;
   int32_t* cols = nullptr;
@@ -285,17 +295,28 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB)
                   int ld, int col0, int nstore, Scratch scr, SolveState* st, int gate, const int32_t* skip, int fin,
                   int fin_arg, const __grid_constant__ BulkCfg bc, int smem_d) {
   extern __shared__ __align__(128) unsigned char bsm[];
-  pdl_wait();
-  pdl_trigger();
-  if (skip && *(volatile const int32_t*)skip) return;
   const bool ing = (gate & GATE_IN_GRAPH) != 0;
   gate &= 0xff;
-  const GateVals gv = gate_load(st, gate);
   Op op = op0;
-  op.scalars(sp);
-  if (!gate_eval(st, gate, ing, gv)) return;
-  const bool last = engine_bulk<NQ, W, R>(geo, op, bsm, bc, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket);
-  if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing, reinterpret_cast<double*>(bsm + bc.base), smem_d);
+  // the CTA's first chunks are requested before the wait for the previous
+  // kernel (they depend on the matrix only); the gate, the scalars and every
+  // vector after it
+  auto sync = [&]() -> bool {
+    pdl_wait();
+    pdl_trigger();
+    if (bc.pdl) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // L1 may hold lines from before the wait
+    if (skip && *(volatile const int32_t*)skip) return false;
+    const GateVals gv = gate_load(st, gate);
+    op.scalars(sp);
+    return gate_eval(st, gate, ing, gv);
+  };
+  const bool last =
+      engine_bulk<NQ, W, R>(geo, op, bsm, bc, part, ld, col0, nstore, scr, st ? &st->ticket : scr.ticket, sync);
+  if (last && fin != FIN_NONE && st) {
+    PK_BTA((size_t)1024 * 32);
+    finalize(st, fin, fin_arg, ing, reinterpret_cast<double*>(bsm + bc.base), smem_d);
+    PK_BTA((size_t)1024 * 32 + 1);
+  }
 }
 
 // One warp per CTA, one unit per warp (CHAIN mapping with group_size >= 32).
@@ -456,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 4)
   if (s_last && fin != FIN_NONE && st && tid < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
 }
 
+#ifdef PK_TILE_ENGINE  // experimental (measured 3-4x slower than the CTA engine on C2), compiled out by default
 // ---------------------------------------------------------------------------
 // TILE engine: rows at streaming speed, each group folded by the CTA that
 // completes it (SpMV operators on CHAIN geometries, group_size % 256 == 0)
@@ -602,6 +624,105 @@ __global__ void __launch_bounds__(256, PK_TILE_MINB)
   __syncthreads();
   if (s_last && fin != FIN_NONE && st && tid < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
 }
+
+#endif  // PK_TILE_ENGINE
+
+// ---------------------------------------------------------------------------
+// VEC row sums: sub-warp-cooperative SpMV rows for long-row matrices
+// ---------------------------------------------------------------------------
+//
+// CSR-adaptive handling of long rows (avg >= vec_min_avg entries): instead of
+// one thread walking a 40- or 400-entry row kSlots entries per dependent
+// round trip, L = 2^lg lanes (8..32, from the average row length) own a row
+// and walk it 4 L entries per round: lane i loads entries c0 + u L + i (u <
+// 4; coalesced columns / values), issues the 4 gathers, and parks the
+// products in a per-warp tile; the row's first lane then adds the round's
+// products in stored order -- acc = ((0 + v0 x0) + v1 x1) + ..., exactly the
+// thread-per-row sum (_spmvkernels.py:12-18).  One pair of dependent round
+// trips per 4 L entries instead of per kSlots.  The sums go to a buffer; the
+// fused operator then runs as an elementwise operator (OpPre) on any
+// reduction engine.  Same IEEE operations in the same order: bit-identical.
+constexpr int kVecWarps = 8;
+constexpr int kVecU = 4;  // entries per lane per round
+template <class Op>
+__global__ void __launch_bounds__(32 * kVecWarps)
+    k_rowsum_warp(int64_t n, const __grid_constant__ Op op0, ScalarPtrs sp, double* __restrict__ qout,
+                  SolveState* st, int gate, const int32_t* skip, int lg) {
+  __shared__ double tile[kVecWarps][kVecU * 32];
+  pdl_wait();
+  pdl_trigger();
+  if (skip && *(volatile const int32_t*)skip) return;
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  const GateVals gv = gate_load(st, gate);
+  Op op = op0;
+  op.scalars(sp);
+  if (!gate_eval(st, gate, ing, gv)) return;
+  using RowT = typename Op::RowT;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int L = 1 << lg, li = lane & (L - 1), sub = lane >> lg;  // lane i of row `sub` of the warp
+  const int RE = kVecU * L;                                         // entries per row per round
+  double* T = tile[wl] + sub * RE;
+  const int rpw = 32 >> lg;
+  const int64_t nblk = (n + rpw - 1) / rpw;
+  for (int64_t blk = (int64_t)blockIdx.x * kVecWarps + wl; blk < nblk; blk += (int64_t)gridDim.x * kVecWarps) {
+    const int64_t row = blk * rpw + sub;
+    RowT b = 0, e = 0;
+    if (row < n) {
+      b = __ldg(op.A.rp + row);
+      e = __ldg(op.A.rp + row + 1);
+    }
+    const int len = (int)(e - b);
+    int mx = len;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    double acc = 0.0;
+    for (int c0 = 0; c0 < mx; c0 += RE) {
+      int32_t col[kVecU];
+      double val[kVecU];
+      bool ok[kVecU];
+#pragma unroll
+      for (int u = 0; u < kVecU; ++u) {
+        const RowT k = b + c0 + u * L + li;
+        ok[u] = k < e;
+        col[u] = ok[u] ? __ldg(op.A.ci + k) : 0;
+        val[u] = ok[u] ? __ldg(op.A.va + k) : 0.0;
+      }
+      typename Op::Gat g[kVecU];
+#pragma unroll
+      for (int u = 0; u < kVecU; ++u) op.gload((uint32_t)col[u], g[u]);
+#pragma unroll
+      for (int u = 0; u < kVecU; ++u) T[u * L + li] = ok[u] ? mul_rn(val[u], op.gval(g[u])) : 0.0;
+      __syncwarp();
+      if (li == 0) {
+        const int cnt = len - c0 < RE ? len - c0 : RE;
+        for (int j = 0; j < cnt; ++j) acc = add_rn(acc, T[j]);
+      }
+      __syncwarp();
+    }
+    if (li == 0 && row < n) qout[row] = acc;
+  }
+}
+
+// The fused operator with its SpMV row sum taken from the VEC buffer: an
+// elementwise operator for the reduction engines (kSpmv = false).
+template <class Op>
+struct OpPre {
+  static constexpr bool kSpmv = false;
+  static constexpr int kMinBlocks = Op::kMinBlocks;
+  Op in;
+  const double* q;
+  struct Item { typename Op::Item it; double q; };
+  __device__ __forceinline__ void load(uint32_t row, Item& t) const {
+    in.load(row, t.it);
+    t.q = __ldg(q + row);
+  }
+  template <int M>
+  __device__ __forceinline__ void compute(uint32_t row, Item& t, double (&c)[M]) const {
+    in.compute(row, t.it, t.q, c);
+  }
+  __device__ __forceinline__ void scalars(const ScalarPtrs& sp) { in.scalars(sp); }
+};
 
 template <class Op>
 __global__ void __launch_bounds__(256, 4) k_sweep(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
@@ -870,6 +991,19 @@ static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
   return PK_OK;
 }
 
+// the VEC pre-pass buffer (n doubles) for a long-row matrix; outside any
+// graph capture (solver set-up, kernel-level entries)
+static int ensure_vec(pk_ctx* c, const pk_mat* a) {
+  if (!a || !a->vec_rows || (size_t)a->n_rows <= c->vec_cap) return PK_OK;
+  PK_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->vecbuf) cudaFree(c->vecbuf);
+  c->vecbuf = nullptr;
+  c->vec_cap = 0;
+  PK_CUDA(cudaMalloc(&c->vecbuf, (size_t)a->n_rows * sizeof(double)));
+  c->vec_cap = (size_t)a->n_rows;
+  return PK_OK;
+}
+
 static Scratch scratch_of(const pk_ctx* c) { return Scratch{c->spill, c->gtick, c->ticket}; }
 
 // Raise a kernel's dynamic shared-memory limit when a launch needs more than
@@ -930,6 +1064,22 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
     return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
   if (geo.leaf && geo.logf > 0 && (size_t)geo.units * 32 * NQ > c->spill_cap)
     return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
+  if constexpr (Op::kSpmv) {
+    if constexpr (!std::decay_t<decltype(op.A)>::kSell && std::is_same<typename Op::RowT, int32_t>::value) {
+      if (op.A.vec && c->vecbuf && c->vec_cap >= (size_t)n) {
+        // long rows: warp-cooperative row sums, then the operator as an
+        // elementwise reduction over them
+        auto kv = k_rowsum_warp<Op>;
+        const int64_t rpb = (int64_t)(32 >> op.A.vec) * kVecWarps;  // rows per CTA pass
+        const int grid = engine_grid(c, kv, 0, (n + rpb - 1) / rpb, 32 * kVecWarps);
+        cudaError_t e = launch_k(c->pdl, kv, dim3((unsigned)grid), dim3(32 * kVecWarps), 0, s, n, op, sp, c->vecbuf,
+                                 st, gate, skip, (int)op.A.vec);
+        if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("VEC row-sum launch: ") + cudaGetErrorString(e));
+        OpPre<Op> pre{op, c->vecbuf};
+        return launch_reduce<NQ>(c, s, n, pre, sp, part, ld, col0, st, gate, skip, fin, fin_arg, nstore);
+      }
+    }
+  }
   if constexpr (Op::kSpmv && NQ <= 4) {
     if (mat_applies(c, geo) && c->mat_cap >= (size_t)n * (size_t)nstore) {
       auto kr = k_mat_rows<NQ, Op>;
@@ -965,6 +1115,7 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
       return PK_OK;
     }
   }
+#ifdef PK_TILE_ENGINE
   if constexpr (Op::kSpmv && NQ <= 4) {
     if (tiles_apply(c, geo) && c->mat && c->mat_cap >= (size_t)n * (size_t)nstore) {
       auto kt = k_reduce_tiles<NQ, Op>;
@@ -980,18 +1131,22 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
       return PK_OK;
     }
   }
-  if constexpr (Op::kSpmv && NQ <= 4) {
-    if constexpr (!std::decay_t<decltype(op.A)>::kSell) {
-      if (c->bulk && !geo.leaf && geo.gs >= 32 && geo.K >= c->bulk_mink && geo.K <= c->bulk_maxk && op.A.blk >= 0) {
+#endif
+  if constexpr (Op::kSpmv && NQ <= 2) {
+    if constexpr (!std::decay_t<decltype(op.A)>::kSell && std::is_same<typename Op::RowT, int32_t>::value) {
+      if (c->bulk && !geo.leaf && geo.gs >= 32 && geo.K >= c->bulk_mink && geo.K <= c->bulk_maxk && NQ <= c->bulk_maxq &&
+          op.A.blk >= 0) {
         constexpr int W = PK_BULK_W, R = PK_BULK_R;
-        const BulkCfg bc = bulk_cfg<NQ, W, R, Op>(op.A.blk);
+        BulkCfg bc = bulk_cfg<NQ, W, R, Op>(op.A.blk);
+        const bool pdl = c->pdl || c->bulk_pdl;
+        bc.pdl = pdl ? 1 : 0;
         const size_t tail = std::max(warp_chain_smem_bytes(geo, NQ), (size_t)kWarpStage2Doubles * sizeof(double));
         const size_t smem = std::max((size_t)bc.total, (size_t)bc.base + tail);
         if (smem <= 100 * 1024 && op.A.maxr <= Op::kSlots) {
           auto kb = k_reduce_bulk<NQ, W, R, PK_BULK_MINB, Op>;
           PK_TRY(allow_dynamic_smem(kb, smem));
           const int smem_d = (int)((smem - bc.base) / sizeof(double));
-          cudaError_t e = launch_k(c->pdl, kb, dim3((unsigned)geo.units), dim3(32 * (W + 1)), smem, s, geo, op, sp,
+          cudaError_t e = launch_k(pdl, kb, dim3((unsigned)geo.units), dim3(32 * (W + 1)), smem, s, geo, op, sp,
                                    part, ld, col0, nstore, scratch_of(c), st, gate, skip, fin, fin_arg, bc, smem_d);
           if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("bulk engine launch: ") + cudaGetErrorString(e));
           return PK_OK;
@@ -1074,6 +1229,18 @@ constexpr int kSweepPairs = PK_SWEEP_PAIRS;  // row pairs per thread of k_sweep2
 template <class Op>
 static int launch_sweep(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, ScalarPtrs sp = ScalarPtrs{},
                         SolveState* st = nullptr, int gate = GATE_NONE) {
+  if constexpr (Op::kSpmv) {
+    if constexpr (!std::decay_t<decltype(op.A)>::kSell && std::is_same<typename Op::RowT, int32_t>::value) {
+      if (op.A.vec && c->vecbuf && c->vec_cap >= (size_t)n) {
+        auto kv = k_rowsum_warp<Op>;
+        const int64_t rpb = (int64_t)(32 >> op.A.vec) * kVecWarps;
+        const int grid = engine_grid(c, kv, 0, (n + rpb - 1) / rpb, 32 * kVecWarps);
+        PK_CUDA(launch_k(c->pdl, kv, dim3((unsigned)grid), dim3(32 * kVecWarps), 0, s, n, op, sp, c->vecbuf, st, gate,
+                         (const int32_t*)nullptr, (int)op.A.vec));
+        return launch_sweep(c, s, n, OpPre<Op>{op, c->vecbuf}, sp, st, gate);
+      }
+    }
+  }
   if constexpr (HasVec2<Op>::value) {
     if (!c->sweep_scalar && op.aligned16()) {
       constexpr int UP = SweepPairs<Op>::value > 0 ? SweepPairs<Op>::value : kSweepPairs;
@@ -1098,6 +1265,11 @@ static Csr<RowT, SELL> csr_of(const pk_mat* a) {
   Csr<RowT, SELL> A{(const RowT*)a->rowptr, a->cols, a->vals};
   A.blk = (int32_t)std::min<int64_t>(a->blk_max, INT32_MAX);
   A.maxr = (int32_t)std::min<int64_t>(a->max_row, INT32_MAX);
+  // VEC pre-pass lanes per row (log2): about a quarter of the average row length, 8..32
+  if (a->vec_rows) {
+    const int64_t avg = a->nnz / std::max<int64_t>(a->n_rows, 1);
+    A.vec = avg >= 96 ? 5 : (avg >= 48 ? 4 : 3);
+  }
   if constexpr (SELL) {
     A.sp = (const RowT*)a->sell_ptr;
     A.sc = a->sell_cols;
@@ -1387,7 +1559,10 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e10 = getenv("PK_WS_CACHE")) c->ws_cache_on = atoi(e10) != 0;
   if (const char* e12 = getenv("PK_LANE")) c->lane_engine = atoi(e12) != 0;
   if (const char* e19 = getenv("PK_TILE_MINK")) c->tile_mink = atoi(e19);
+  if (const char* e23 = getenv("PK_VEC_MINAVG")) c->vec_min_avg = atoi(e23);
   if (const char* e16 = getenv("PK_BULK")) c->bulk = atoi(e16) != 0;
+  if (const char* e21 = getenv("PK_BULK_PDL")) c->bulk_pdl = atoi(e21) != 0;
+  if (const char* e22 = getenv("PK_BULK_MAXQ")) c->bulk_maxq = atoi(e22);
   if (const char* e20 = getenv("PK_BULK_MAXK")) c->bulk_maxk = atoi(e20);
   if (const char* e17 = getenv("PK_BULK_MINK")) c->bulk_mink = std::max(2, atoi(e17));
   if (const char* e15 = getenv("PK_GS_SPLIT")) c->gs_split = atoi(e15) != 0;
@@ -1418,6 +1593,7 @@ extern "C" int pk_ctx_destroy(pk_ctx* c) {
   if (c->gtick) cudaFree(c->gtick);
   if (c->spill) cudaFree(c->spill);
   if (c->mat) cudaFree(c->mat);
+  if (c->vecbuf) cudaFree(c->vecbuf);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return PK_OK;
@@ -1862,6 +2038,8 @@ static int compute_blk_max(pk_ctx* c, pk_mat* m) {
 
 static int apply_default_format(pk_ctx* c, pk_mat* m) {
   PK_TRY(compute_blk_max(c, m));
+  m->vec_rows = c->vec_min_avg > 0 && !m->row64 && m->n_rows > 0 && m->nnz >= (int64_t)c->vec_min_avg * m->n_rows;
+  if (m->vec_rows) return PK_OK;  // long rows: CSR + VEC pre-pass rather than SELL-32
   const bool want = c->sell_mode == 1 ||
                     (c->sell_mode == 2 && m->n_rows >= (int64_t(1) << 19) && m->nnz >= 12 * m->n_rows && !m->row64);
   return want ? pk_mat_set_format(c, m, PK_FMT_SELL32) : PK_OK;
@@ -1889,6 +2067,7 @@ extern "C" int pk_spmv(pk_ctx* c, const pk_mat* a, const double* p, double* q) {
   PK_CHECK_CTX(c);
   if (!a || (!p && a->n_cols) || (!q && a->n_rows)) return fail(PK_ERR_INVALID, "NULL argument");
   if (a->n_rows == 0) return PK_OK;
+  PK_TRY(ensure_vec(c, a));
   return spmv_fused_any(c, c->stream, a, p, q, 0, nullptr, nullptr, nullptr, 0, 0);
 }
 
@@ -1993,6 +2172,7 @@ extern "C" int pk_spmv_fused(pk_ctx* c, const pk_mat* a, const double* p, double
     if (kinds[k] == PK_DOT_VECTOR && (!w || !w[k])) return fail(PK_ERR_INVALID, "missing fixed dot vector");
   }
   PK_TRY(ensure_scratch(c, a->n_rows, nq));
+  PK_TRY(ensure_vec(c, a));
   return spmv_fused_any(c, c->stream, a, p, q, nq, kinds, w, partials, nq, 0);
 }
 

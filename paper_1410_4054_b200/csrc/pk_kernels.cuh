@@ -165,39 +165,39 @@ struct S2Col {
 
 template <int NC>
 __device__ __noinline__ void stage2_warp(const S2Col* cols, int ng, double* out, double* buf, int buf_d) {
-  const int CH = buf_d / NC;  // groups per chunk of the (dynamic) staging buffer
+  // groups per staged chunk: up to 128 (4 per lane per column), all of a
+  // chunk's loads in flight before its shared-memory stores (one L2 round
+  // trip per chunk instead of one per element)
+  constexpr int UPL = 4;
+  int CH = buf_d / NC;
+  CH = CH < 32 * UPL ? CH : 32 * UPL;
   const int lane = threadIdx.x & 31;
+  const double* cp[NC];
+  int cld[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    cp[c] = cols[c].part + cols[c].col;
+    cld[c] = cols[c].ld;
+  }
   double tot = 0.0;
   for (int g0 = 0; g0 < ng; g0 += CH) {
     const int cnt = (ng - g0) < CH ? (ng - g0) : CH;
     __syncwarp();
-#if PK_S2_SU > 0
-    // PK_S2_SU loads per lane in flight before the shared-memory stores
-    for (int base = 0; base < cnt * NC; base += 32 * PK_S2_SU) {
-      double v[PK_S2_SU];
+    double v[NC][UPL];
 #pragma unroll
-      for (int u = 0; u < PK_S2_SU; ++u) {
-        const int idx = base + u * 32 + lane;
-        if (idx < cnt * NC) {
-          const int c = idx / cnt, g = idx - c * cnt;
-          v[u] = __ldcg(cols[c].part + (int64_t)(g0 + g) * cols[c].ld + cols[c].col);
-        }
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int u = 0; u < UPL; ++u) {
+        const int g = u * 32 + lane;
+        v[c][u] = g < cnt ? __ldcg(cp[c] + (int64_t)(g0 + g) * cld[c]) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < PK_S2_SU; ++u) {
-        const int idx = base + u * 32 + lane;
-        if (idx < cnt * NC) {
-          const int c = idx / cnt, g = idx - c * cnt;
-          buf[c * CH + g] = v[u];
-        }
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int u = 0; u < UPL; ++u) {
+        const int g = u * 32 + lane;
+        if (g < cnt) buf[c * CH + g] = v[c][u];
       }
-    }
-#else
-    for (int idx = lane; idx < cnt * NC; idx += 32) {
-      const int c = idx / cnt, g = idx - c * cnt;
-      buf[c * CH + g] = __ldcg(cols[c].part + (int64_t)(g0 + g) * cols[c].ld + cols[c].col);
-    }
-#endif
     __syncwarp();
     if (lane < NC) {
       const double* b = buf + lane * CH;

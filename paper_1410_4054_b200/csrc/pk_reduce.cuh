@@ -148,6 +148,7 @@ struct Csr {
   const double* sv = nullptr;
   int32_t blk = -1;           // host: most entries in an aligned 32-row block (BULK engine slot size), -1 unknown
   int32_t maxr = 0;           // host: longest row
+  int32_t vec = 0;            // host: long-row matrix -- SpMV row sums by the warp-cooperative VEC pre-pass
 };
 
 // [b, e) walk of a row and the slot stride: CSR (rp[row], rp[row + 1], 1) or
@@ -799,16 +800,28 @@ __device__ __forceinline__ void group_tree_warp(const Geom& geo, int g, const do
   const int mm = geo.gs / 32;
   const int lg = ilog2_u((uint32_t)mm);
   LeafStack<NQ> st{stk, 32, lane};
-  for (int i = 0; i < mm; ++i) {
-    const int64_t idx = base + (int64_t)brev_bits((uint32_t)i, lg) * 32 + lane;
-    double x[NQ];
+  // the leaves' loads go out in batches of 8 (one L2 round trip per batch,
+  // not per leaf), then the pushes in visit order
+  constexpr int BL = 8;
+  for (int i0 = 0; i0 < mm; i0 += BL) {
+    double x[BL][NQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) x[q] = q < nstore ? __ldcg(spill + (int64_t)q * geo.G + idx) : 0.0;
-    if (mm > 1) {
-      st.push((uint32_t)i, x, v);
-    } else {
+    for (int b = 0; b < BL; ++b) {
+      const int i = i0 + b;
+      const int64_t idx = base + (int64_t)brev_bits((uint32_t)(i < mm ? i : 0), lg) * 32 + lane;
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) v[q] = x[q];
+      for (int q = 0; q < NQ; ++q) x[b][q] = (q < nstore && i < mm) ? __ldcg(spill + (int64_t)q * geo.G + idx) : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < BL; ++b) {
+      const int i = i0 + b;
+      if (i >= mm) break;
+      if (mm > 1) {
+        st.push((uint32_t)i, x[b], v);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v[q] = x[b][q];
+      }
     }
   }
 #pragma unroll

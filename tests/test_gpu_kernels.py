@@ -248,3 +248,28 @@ def test_spmv_fused_empty_and_long_rows(pk, fused, geom):
         dm = pk.DeviceMatrix.upload(pk.context_for(ctx), a).set_format(fmt, ctx)
         q, part = fused.spmv_fused(dm, dev(p), ("input", "result", dev(w)), ctx)
         assert same(host(q), oq) and same(host(part), opart), fmt
+
+
+@pytest.mark.parametrize("geom", [(16, 64), (4, 256), (128, 256), (2, 4096)])
+def test_spmv_fused_vec_rows(pk, fused, geom):
+    """Long-row matrix (avg >= 24 entries per row): the SpMV row sums come
+    from the warp-cooperative VEC pre-pass (k_rowsum_warp) and the fused
+    operator runs as an elementwise reduction over them -- bitwise vs the
+    oracle, with empty rows, a 700-entry row and rows longer than 32."""
+    rng = np.random.default_rng(11)
+    n = 3000
+    lens = rng.integers(10, 50, n)
+    lens[rng.random(n) < 0.05] = 0
+    lens[7] = 700
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens])
+    vals = rng.standard_normal(rows.size)
+    a = pk.CsrMatrix.from_coo(n, n, rows, cols, vals)
+    assert a.nnz >= 24 * n
+    p, w = rng.standard_normal(n), rng.standard_normal(n)
+    ctx = pk.ExecutionContext(*geom)
+    oq, opart = orc.spmv_fused(a, p, ("input", "result", w), geom)
+    dm = pk.DeviceMatrix.upload(pk.context_for(ctx), a)
+    q, part = fused.spmv_fused(dm, dev(p), ("input", "result", dev(w)), ctx)
+    assert same(host(q), oq) and same(host(part), opart)
+    assert same(host(fused.spmv_csr(dm, dev(p), ctx)), oq)  # plain SpMV: VEC pre-pass + elementwise sweep

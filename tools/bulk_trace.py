@@ -22,6 +22,7 @@ cfg1 = pk.SolverConfig(fixed_iterations=1, max_iterations=1, loop_mode="host")
 solve_resident("bicgstab", dm, b, config=cfg1, context=ctx)
 torch.cuda.synchronize()
 lib.pk_debug_bulk_trace(ctypes.c_void_p(0))
+fin = buf[1024 * 32: 1024 * 32 + 2].cpu().numpy()
 t = buf[: 1024 * 32].view(1024, 32).cpu().numpy()
 # the last bulk launch overwrote the buffer: ApNext (2nd SpMV) -- report it
 t0 = t[:, 0].min()
@@ -34,6 +35,8 @@ for j in range(8):
     out[f"chunk{j}_full"] = st(t[:, 5 + 2 * j] - t0)
     out[f"chunk{j}_computed"] = st(t[:, 21 + j] - t0)
     out[f"chunk{j}_end"] = st(t[:, 6 + 2 * j] - t0)
+out["finalizer_start"] = float(fin[0] - t0)
+out["finalizer_end"] = float(fin[1] - t0)
 sm = t[:, 3]
 out["ctas_per_sm"] = np.bincount(sm.astype(np.int64)).tolist()[:8]
 out["distinct_sms"] = int(len(set(sm.tolist())))
