@@ -767,6 +767,15 @@ __global__ void __launch_bounds__(256) k_sweep2(int64_t n, Op op, ScalarPtrs sp,
   }
 }
 
+// Profiling aid (PK_FLAG_PROFILE host loops): hold the stream for `cycles`
+// SM clocks so the host enqueues the whole batch behind it; the per-kernel
+// event brackets then time back-to-back kernels, not the host's launch rate.
+__global__ void k_spin(long long cycles) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {
+  }
+}
+
 __global__ void k_finalize(SolveState* st, int fin, int arg) {
   __shared__ double buf[1024];
   finalize(st, fin, arg, false, buf, 1024);
