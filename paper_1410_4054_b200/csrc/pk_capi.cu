@@ -1191,7 +1191,10 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
     const size_t wsm = std::max(warp_chain_smem_bytes(geo, NQ), (size_t)kWarpStage2Doubles * sizeof(double));
     auto kw = k_reduce_warp<NQ, R, Op>;
     PK_TRY(allow_dynamic_smem(kw, wsm));
-    cudaError_t e = launch_k(c->pdl, kw, dim3((unsigned)geo.units), dim3(32), wsm, s, geo, op, sp, part, ld, col0,
+    // grid-stride over the units, capped at the context's SM budget (batch
+    // workers run many small solves side by side)
+    const int wgrid = engine_grid(c, kw, wsm, geo.units, 32);
+    cudaError_t e = launch_k(c->pdl, kw, dim3((unsigned)wgrid), dim3(32), wsm, s, geo, op, sp, part, ld, col0,
                              nstore, scratch_of(c), st, gate, skip, fin, fin_arg);
     if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("warp engine launch: ") + cudaGetErrorString(e));
     return PK_OK;
