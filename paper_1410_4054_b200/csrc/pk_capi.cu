@@ -119,12 +119,14 @@ struct pk_ctx {
   bool staged = true;             // PK_STAGE=0: off (only in -DPK_STAGED_ENGINE builds: the cp.async-staged
                                   // CHAIN engine, measured slower; compiling it in also slows the default engine)
   int sell_mode = 2;              // PK_SELL: 0 never / 1 always / 2 auto -- new matrices get a SELL-32 copy the kernels
-                                  // walk when n >= 2^19 and nnz >= 12 n (measured: random 16/row, n = 1M: CG 344 -> 260
-                                  // us/iter; stencils (5-7/row) and short matrices gain nothing or lose)
+                                  // walk when n >= 2^19 and nnz >= 12 n and the VEC pre-pass is off (measured: random
+                                  // 16/row, n = 1M: CG 344 -> 260 us/iter; VEC 216); stencils (5-7/row) stay on CSR
   bool sweep_scalar = false;      // PK_SWEEP_SCALAR=1: scalar grid-stride sweeps instead of the 16-byte k_sweep2
   int tile_mink = 0;              // PK_TILE_MINK: shortest lane chain (K) sent to the TILE engine (0 = off; experimental)
-  int vec_min_avg = 24;           // PK_VEC_MINAVG: matrices with >= this many entries per row on average take the VEC
-                                  // row-sum pre-pass (0 = off)
+  int vec_min_avg = 12;           // PK_VEC_MINAVG: matrices with >= this many entries per row on average take the VEC
+                                  // row-sum pre-pass (0 = off).  Measured (CG / BiCGStab us/iter, VEC vs SELL-32 vs
+                                  // thread-per-row): 16/row n = 1M 216 / 254 / 338, 454 / 571 / 726; 40/row n = 200k
+                                  // 116 / 256 / 165; 400/row n = 20k 90 / 409 / 155
   double* vecbuf = nullptr;       // its row sums, vec_cap doubles
   size_t vec_cap = 0;
   bool bulk = true;               // PK_BULK=0: SpMV operators on long lane chains use the CTA CHAIN engine instead of
@@ -220,6 +222,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
 
 #ifndef PK_LANE_D_WIDE
 #define PK_LANE_D_WIDE 4
+#endif
+#ifndef PK_LANE_D_LIGHT
+#define PK_LANE_D_LIGHT 16  // chunks in flight per lane for items of <= 2 doubles (dots, normalize)
 #endif
 
 // LANE engine kernel (elementwise operators on CHAIN geometries): one thread
@@ -633,7 +638,7 @@ __global__ void __launch_bounds__(256, PK_TILE_MINB)
 //
 // CSR-adaptive handling of long rows (avg >= vec_min_avg entries): instead of
 // one thread walking a 40- or 400-entry row kSlots entries per dependent
-// round trip, L = 2^lg lanes (8..32, from the average row length) own a row
+// round trip, L = 2^lg lanes (4..32, from the average row length) own a row
 // and walk it 4 L entries per round: lane i loads entries c0 + u L + i (u <
 // 4; coalesced columns / values), issues the 4 gathers, and parks the
 // products in a per-warp tile; the row's first lane then adds the round's
@@ -1113,7 +1118,7 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
       // rows (dots, normalize, updates) need many chunks to cover a latency,
       // wide ones (multi-dot, Gram-Schmidt) few (registers)
       constexpr size_t IB = sizeof(typename Op::Item);
-      constexpr int D = IB <= 32 ? 16 : (IB <= 64 ? 8 : (IB <= 160 ? PK_LANE_D_WIDE : 2));
+      constexpr int D = IB <= 16 ? PK_LANE_D_LIGHT : (IB <= 32 ? 16 : (IB <= 64 ? 8 : (IB <= 160 ? PK_LANE_D_WIDE : 2)));
       const int T = lane_cta_threads(geo);
       const int sd = (int)std::max<size_t>(std::max<size_t>(engine_tail_doubles(geo, NQ), (size_t)NQ * T), 1024);
       auto kl = k_reduce_lane<NQ, D, Op>;
@@ -1277,10 +1282,10 @@ static Csr<RowT, SELL> csr_of(const pk_mat* a) {
   Csr<RowT, SELL> A{(const RowT*)a->rowptr, a->cols, a->vals};
   A.blk = (int32_t)std::min<int64_t>(a->blk_max, INT32_MAX);
   A.maxr = (int32_t)std::min<int64_t>(a->max_row, INT32_MAX);
-  // VEC pre-pass lanes per row (log2): about a quarter of the average row length, 8..32
+  // VEC pre-pass lanes per row (log2): about a quarter of the average row length, 4..32
   if (a->vec_rows) {
     const int64_t avg = a->nnz / std::max<int64_t>(a->n_rows, 1);
-    A.vec = avg >= 96 ? 5 : (avg >= 48 ? 4 : 3);
+    A.vec = avg >= 96 ? 5 : (avg >= 48 ? 4 : (avg >= 24 ? 3 : 2));
   }
   if constexpr (SELL) {
     A.sp = (const RowT*)a->sell_ptr;

@@ -1006,7 +1006,10 @@ __device__ __forceinline__ bool engine_warp_chain(const Geom& geo, const Op& op,
 // the whole group (T == gs); otherwise lane values go to the spill buffer and
 // the CTA completing the group runs group_tree().  Global ticket + finalizer as
 // in engine_run().
-constexpr int kLaneThreads = 256;
+#ifndef PK_LANE_THREADS
+#define PK_LANE_THREADS 256
+#endif
+constexpr int kLaneThreads = PK_LANE_THREADS;
 
 __host__ __device__ inline int lane_cta_threads(const Geom& g) { return g.gs < kLaneThreads ? g.gs : kLaneThreads; }
 

@@ -1,7 +1,7 @@
 """Format experiment: CSR vs SELL-32 walk for short (stencil) and long
 (unstructured, gen_random_rowwise) rows; per-iteration graph time of a
 fixed-iteration pipelined solve, same bits either way.  CSR matrices with
->= PK_VEC_MINAVG entries per row (default 24) take the warp-cooperative VEC
+>= PK_VEC_MINAVG entries per row (default 12) take the warp-cooperative VEC
 row-sum pre-pass; run with PK_VEC_MINAVG=0 for thread-per-row CSR."""
 import os
 import json
@@ -22,7 +22,7 @@ for fam, n, k in cases:
     a, b = pk.gen_random_rowwise(n, k, seed=1)
     for method in ("cg", "bicgstab"):
         out = {"matrix": f"{fam} n={n} k={k}", "method": method,
-               "csr_walk": "vec" if k >= int(os.environ.get("PK_VEC_MINAVG", "24")) > 0 else "thread-per-row"}
+               "csr_walk": "vec" if k >= int(os.environ.get("PK_VEC_MINAVG", "12")) > 0 else "thread-per-row"}
         xs = {}
         for fmt in ("csr", "sell32"):
             dm = pk.DeviceMatrix.upload(dc, a).set_format(fmt, ctx)
