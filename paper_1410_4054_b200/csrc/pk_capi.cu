@@ -129,6 +129,8 @@ struct pk_ctx {
                                   // 116 / 256 / 165; 400/row n = 20k 90 / 409 / 155
   double* vecbuf = nullptr;       // its row sums, vec_cap doubles
   size_t vec_cap = 0;
+  bool mdq = false;               // PK_MDQ=1: GMRES multi-dots by k_multidot_q (quantity-parallel; measured slower:
+                                  // GMRES(30) 128^3 multi-dot 98.5 vs 89.3 us, 64^3 51.4 vs 40.5 on the LANE engine)
   bool bulk = true;               // PK_BULK=0: SpMV operators on long lane chains use the CTA CHAIN engine instead of
                                   // the TMA-fed BULK engine (pk_bulk.cuh)
   bool bulk_pdl = false;          // PK_BULK_PDL=1: BULK kernels launch programmatically (their CSR prologue overlaps
@@ -1410,9 +1412,112 @@ static int multidot_nb_cap(const pk_ctx* c, int64_t n) {
 }
 
 // <b_j, v> partials for nb vectors, in passes of at most the smem cap.
+// ---------------------------------------------------------------------------
+// MDQ multi-dot: quantity-parallel Gram-Schmidt coefficients
+// ---------------------------------------------------------------------------
+//
+// c_j = <v_j, w> for the nb basis vectors of a classical Gram-Schmidt step
+// (fused.py:222-243).  The LANE engine gives one thread a lane and ALL nb
+// quantities (nb + 1 loads per chunk, ~200 registers, 32768 threads for the
+// whole GPU); here a warp owns one (32-lane unit, quantity) pair: thread =
+// (lane, q) folds lane t's chain of v_q[row] * w[row] products in chunk
+// order with 16 chunks of loads in flight (the reference order,
+// linalg.py:300-303 -- exactly OpMultiDot's products and adds), the 8 warps
+// of a CTA are 8 quantities of the same 32 lanes (w is read from DRAM once,
+// then hits L1).  Lane values -> spill; the CTA that completes a group (all
+// its units and quantity blocks) runs the group's halving trees, 8
+// quantities at a time; the CTA completing the last group finalizes.
+struct MdqPtrs {
+  const double* p[32];
+};
+constexpr int kMdqD = 16;
+__global__ void __launch_bounds__(256)
+    k_multidot_q(const __grid_constant__ Geom geo, const double* __restrict__ w, const __grid_constant__ MdqPtrs bp,
+                 int nb, double* part, int ld, int col0, Scratch scr, SolveState* st, int gate, int fin, int fin_arg,
+                 int smem_d) {
+  extern __shared__ double smem[];
+  __shared__ int s_flag;
+  __shared__ int s_last;
+  pdl_wait();
+  pdl_trigger();
+  const bool ing = (gate & GATE_IN_GRAPH) != 0;
+  gate &= 0xff;
+  const GateVals gv = gate_load(st, gate);
+  if (!gate_eval(st, gate, ing, gv)) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nqb = (nb + 7) >> 3;
+  const int64_t unit = blockIdx.x / nqb;
+  const int qb = (int)(blockIdx.x - unit * nqb);
+  const int q = qb * 8 + warp;
+  const int64_t t = unit * 32 + lane;  // lane id (< G: the units tile [0, G))
+  const int64_t n = geo.n, G = geo.G, K = geo.K;
+  if (tid == 0) s_last = 0;
+  if (q < nb) {
+    const double* __restrict__ v = bp.p[q];
+    double acc = 0.0;
+    for (int64_t k0 = 0; k0 < K; k0 += kMdqD) {
+      double a[kMdqD], b[kMdqD];
+#pragma unroll
+      for (int d = 0; d < kMdqD; ++d) {
+        const int64_t row = (k0 + d) * G + t;
+        const int64_t rc = row < n ? row : t;  // clamped: every load unconditional
+        a[d] = __ldg(v + rc);
+        b[d] = __ldg(w + rc);
+      }
+#pragma unroll
+      for (int d = 0; d < kMdqD; ++d)
+        if (k0 + d < K && (k0 + d) * G + t < n) acc = add_rn(acc, mul_rn(a[d], b[d]));
+    }
+    scr.spill[(int64_t)q * G + t] = acc;
+  }
+  __syncthreads();
+  const int g = (int)(unit * 32 / geo.gs);
+  if (tid == 0) {
+    const unsigned per = (unsigned)(geo.gs / 32) * (unsigned)nqb;
+    const unsigned tk = ticket_add(scr.gtick + g, 1u);
+    const int last = tk == per - 1;
+    if (last) {
+      scr.gtick[g] = 0u;
+      acquire_fence();
+    }
+    s_flag = last;
+  }
+  __syncthreads();
+  if (s_flag) {
+    for (int q0 = 0; q0 < nb; q0 += 8)
+      group_tree<8>(geo, g, scr.spill + (int64_t)q0 * G, smem, part, ld, col0 + q0, nb - q0 < 8 ? nb - q0 : 8);
+    if (tid == 0) {
+      unsigned* ticket = st ? &st->ticket : scr.ticket;
+      const unsigned tk = ticket_add(ticket, 1u);
+      if (tk + 1u == (unsigned)geo.n_groups) {
+        *ticket = 0u;
+        acquire_fence();
+        s_last = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_last && fin != FIN_NONE && st && tid < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
+}
+
 static int multidot_any(pk_ctx* c, cudaStream_t s, int64_t n, int nb, const double* const* basis,
                         const double* v, double* part, int ld, int col0, SolveState* st = nullptr,
                         int gate = GATE_NONE, int fin = FIN_NONE, int fin_arg = 0) {
+  {
+    const Geom geo = make_geom(n, c->ng, c->gs, min_units(c));
+    if (c->mdq && nb >= 1 && nb <= 32 && !geo.leaf && geo.gs >= 32 && geo.K >= 2 &&
+        (size_t)geo.G * (size_t)nb <= c->spill_cap) {
+      MdqPtrs bp{};
+      for (int j = 0; j < nb; ++j) bp.p[j] = basis[j];
+      const int sd = (int)std::max<size_t>(engine_tail_doubles(geo, 8), 1024);
+      PK_TRY(allow_dynamic_smem(k_multidot_q, (size_t)sd * sizeof(double)));
+      const int64_t grid = geo.units * ((nb + 7) / 8);
+      cudaError_t e = launch_k(c->pdl, k_multidot_q, dim3((unsigned)grid), dim3(256), (size_t)sd * sizeof(double), s,
+                               geo, v, bp, nb, part, ld, col0, scratch_of(c), st, gate, fin, fin_arg, sd);
+      if (e != cudaSuccess) return fail(PK_ERR_CUDA, std::string("MDQ multi-dot launch: ") + cudaGetErrorString(e));
+      return PK_OK;
+    }
+  }
   int cap = multidot_nb_cap(c, n);
   int done = 0;
   while (done < nb) {
@@ -1577,6 +1682,7 @@ extern "C" int pk_ctx_create(int device, int64_t n_groups, int64_t group_size, p
   if (const char* e12 = getenv("PK_LANE")) c->lane_engine = atoi(e12) != 0;
   if (const char* e19 = getenv("PK_TILE_MINK")) c->tile_mink = atoi(e19);
   if (const char* e23 = getenv("PK_VEC_MINAVG")) c->vec_min_avg = atoi(e23);
+  if (const char* e24 = getenv("PK_MDQ")) c->mdq = atoi(e24) != 0;
   if (const char* e16 = getenv("PK_BULK")) c->bulk = atoi(e16) != 0;
   if (const char* e21 = getenv("PK_BULK_PDL")) c->bulk_pdl = atoi(e21) != 0;
   if (const char* e22 = getenv("PK_BULK_MAXQ")) c->bulk_maxq = atoi(e22);
