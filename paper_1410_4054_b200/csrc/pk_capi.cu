@@ -979,6 +979,14 @@ static int mat_discard(const pk_ctx* c, const Geom& geo) {
   return c->mat_discard && geo.n % 32 == 0 && geo.G % 32 == 0 ? 1 : 0;
 }
 
+// Cached solver workspaces hold instantiated graphs whose kernel parameters
+// point into the context's scratch (spill, contribution and VEC buffers):
+// whenever one of those buffers is reallocated the cache is dropped, so no
+// cached graph can ever launch with a freed pointer.
+static void scratch_moved(pk_ctx* c) {
+  if (c->ws_cache_free) c->ws_cache_free(c);
+}
+
 static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
   Geom geo = make_geom(n, c->ng, c->gs, min_units(c));
   if (mat_applies(c, geo) || tiles_apply(c, geo)) {
@@ -986,6 +994,7 @@ static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
     const size_t mneed = (size_t)n * (size_t)std::min(std::max(nq, 1), 4);
     if (mneed > c->mat_cap) {
       PK_CUDA(cudaStreamSynchronize(c->stream));
+      scratch_moved(c);
       if (c->mat) cudaFree(c->mat);
       c->mat = nullptr;
       c->mat_cap = 0;
@@ -999,6 +1008,7 @@ static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
                                 : (size_t)geo.G * (size_t)std::max(nq, 1);
   if (need <= c->spill_cap) return PK_OK;
   PK_CUDA(cudaStreamSynchronize(c->stream));
+  scratch_moved(c);
   if (c->spill) cudaFree(c->spill);
   c->spill = nullptr;
   c->spill_cap = 0;
@@ -1012,6 +1022,7 @@ static int ensure_scratch(pk_ctx* c, int64_t n, int nq) {
 static int ensure_vec(pk_ctx* c, const pk_mat* a) {
   if (!a || !a->vec_rows || (size_t)a->n_rows <= c->vec_cap) return PK_OK;
   PK_CUDA(cudaStreamSynchronize(c->stream));
+  scratch_moved(c);
   if (c->vecbuf) cudaFree(c->vecbuf);
   c->vecbuf = nullptr;
   c->vec_cap = 0;

@@ -429,3 +429,26 @@ def test_gmres_restart_longer_than_one_update_chunk(pk, m):
     cfgf = pk.SolverConfig(restart=m, fixed_iterations=m + 3, max_iterations=m + 3)
     resf = pk.gmres_pipelined(a, b, config=cfgf, context=pk.ExecutionContext(8, 32))
     assert_identical(resf, oracle_run("gmres", a, b, (8, 32), restart=m, fixed=m + 3, max_iterations=m + 3))
+
+
+def test_cached_workspace_survives_scratch_growth(pk):
+    """A cached workspace's graph holds the context's scratch pointers: a later
+    solve on the same context that grows (reallocates) the VEC buffer (a long-
+    row matrix) or the spill (GMRES: 32 lane chains per lane) must drop the
+    cache -- the repeated CG solve is then rebuilt and still bit-identical to
+    its first run and to the oracle."""
+    ctx = pk.ExecutionContext(16, 64)
+    a_small, b_small = pk.gen_poisson2d(4)  # 127^2 rows, 5 per row
+    cfg = pk.SolverConfig(max_iterations=300)
+    first = pk.cg_pipelined(a_small, b_small, config=cfg, context=ctx)
+    big, bb = pk.gen_random_rowwise(60000, 20, seed=4)  # VEC rows (>= 12 per row on average)
+    fixed3 = pk.SolverConfig(fixed_iterations=3, max_iterations=3)
+    for grow in (lambda: pk.cg_pipelined(big, bb, config=fixed3, context=ctx),
+                 lambda: pk.gmres_pipelined(a_small, b_small, config=pk.SolverConfig(fixed_iterations=3,
+                                                                                   max_iterations=3, restart=30),
+                                            context=ctx)):
+        grow()
+        again = pk.cg_pipelined(a_small, b_small, config=cfg, context=ctx)
+        assert again.iterations == first.iterations
+        assert same(again.x, first.x) and same(again.residual_history, first.residual_history)
+    assert_identical(first, oracle_run("cg", a_small, b_small, (16, 64), max_iterations=300))
