@@ -2112,16 +2112,21 @@ extern "C" int pk_mat_set_format(pk_ctx* c, pk_mat* m, int32_t format) {
   if (!c || !m) return fail(PK_ERR_INVALID, "NULL argument");
   if (format != PK_FMT_CSR && format != PK_FMT_SELL32) return fail(PK_ERR_INVALID, "unknown matrix format");
   PK_TRY(set_device(m->device));
+  // a format change gives the matrix a new identity: cached solver
+  // workspaces (keyed by it) hold graphs that walk the old arrays
   if (format == PK_FMT_CSR) {
     if (m->sell) {
       PK_CUDA(cudaStreamSynchronize(c->stream));
       free_sell(m);
+      m->uid = g_mat_uid.fetch_add(1);
     }
     return PK_OK;
   }
   if (m->sell || m->n_rows == 0) return PK_OK;
   if (m->row64) return fail(PK_ERR_UNSUPPORTED, "SELL-32 needs nnz < 2^31 (32-bit offsets)");
-  return build_sell_t<int32_t>(c, m);
+  PK_TRY(build_sell_t<int32_t>(c, m));
+  m->uid = g_mat_uid.fetch_add(1);
+  return PK_OK;
 }
 
 extern "C" int pk_mat_get_format(const pk_mat* m, int32_t* format, int64_t* stored_entries) {

@@ -452,3 +452,24 @@ def test_cached_workspace_survives_scratch_growth(pk):
         assert again.iterations == first.iterations
         assert same(again.x, first.x) and same(again.residual_history, first.residual_history)
     assert_identical(first, oracle_run("cg", a_small, b_small, (16, 64), max_iterations=300))
+
+
+def test_cached_workspace_survives_format_change(pk):
+    """Switching a device matrix between SELL-32 and CSR frees / builds the
+    SELL copy that cached graphs may walk: the matrix takes a new identity,
+    so the next solve builds a fresh workspace; results stay bit-identical."""
+    from paper_1410_4054_b200.solvers import solve_resident
+
+    ctx = pk.ExecutionContext(16, 64)
+    dc = pk.context_for(ctx)
+    a, b = pk.gen_random_rowwise(20000, 8, seed=2)
+    dm = pk.DeviceMatrix.upload(dc, a)
+    bt = torch.from_numpy(np.asarray(b)).cuda()
+    cfg = pk.SolverConfig(fixed_iterations=20, max_iterations=20)
+    runs = []
+    for fmt in ("sell32", "csr", "sell32", "csr"):
+        dm.set_format(fmt, ctx)
+        x, r = solve_resident("cg", dm, bt, config=cfg, context=ctx)
+        runs.append((x.cpu().numpy(), list(r.residual_history)))
+    for x, h in runs[1:]:
+        assert same(x, runs[0][0]) and same(h, runs[0][1])
