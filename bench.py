@@ -341,6 +341,36 @@ def kernel_roofline(pk, dm, ctx, b, iters=200):
             "kernels": rows}
 
 
+def roofline_wide(pk, b_host, iters=200):
+    """The parity tax of the reference geometry: the same C2 system at the
+    one-element-per-lane geometry 128 x 8192 (G = n, K = 1: LEAF engine, no
+    lane chains) -- different reduction geometry, so different roundings; a
+    performance comparison only."""
+    from paper_1410_4054_b200.solvers import solve_resident
+    import torch
+
+    wide = pk.ExecutionContext(128, 8192)
+    dm, _ = pk.convdiff2d(SIDE, device=True, context=wide)
+    b = torch.from_numpy(b_host).to("cuda")
+    n = dm.n_rows
+    g = pk.SolverConfig(fixed_iterations=iters, max_iterations=iters)
+    solve_resident("bicgstab", dm, b, config=g, context=wide)
+    _, rg = solve_resident("bicgstab", dm, b, config=g, context=wide)
+    us = rg.loop_seconds / iters * 1e6
+    r = kernel_roofline(pk, dm, wide, b, iters)
+    iter_bytes = 2 * b_csr(n, dm.nnz) + 128 * n
+    peak, _ = peaks()
+    return {"geometry": "128x8192 (the headline's 128 groups, one element per lane: LEAF engine)", "us_per_iter": round(us, 3),
+            "iteration_frac": round(iter_bytes / (us * 1e-6) / 1e9 / peak, 4),
+            "dominant_kernel_us": r["us_per_launch"], "dominant_kernel_frac": r["frac"],
+            "kernels": [{"kernel": name, "us_per_launch": row["us_per_launch"], "achieved": row["achieved"]}
+                        for name, row in zip(("As = A s + 4 dots (LEAF engine)", "Ap' = A p' + 2 dots (LEAF engine)",
+                                              "xrp sweep"), r["kernels"])],
+            "note": "same system at a geometry whose lanes hold one row each (no lane chains; LEAF engine): "
+                    "what reproducing the reference's 128 x 256 chains bit for bit costs or saves relative to "
+                    "the other ordering the reference could be run with"}
+
+
 def classical_same_box(pk, method, a, b, ctx, pipelined_us, iters=40):
     """The reference's classical driver (one kernel per BLAS op, a host read
     per inner product; solvers.py:310-389 / 485-580) on the same B200 and the
@@ -520,6 +550,10 @@ def run_c2(args, torch, pk, dev):
     }
     a_host, bh = pk.convdiff2d(SIDE)
     line["classical_gpu"] = classical_same_box(pk, "bicgstab", a_host, bh, ctx, us_iter)
+    try:
+        line["roofline_wide"] = roofline_wide(pk, b_host)
+    except Exception as exc:  # informational only
+        line["roofline_wide"] = {"error": str(exc)[:200]}
     return line
 
 

@@ -961,7 +961,9 @@ static int64_t min_units(const pk_ctx* c) { return (int64_t)c->sm_count * 4; }
 // zero-fill unit skips the empty groups (n = 225: 12.5 vs 16.5 us/iter).
 // PK_WARP_K1=0 turns it off.
 static bool warp_k1(const pk_ctx* c, const Geom& geo) {
-  return c->warp_k1 && geo.G <= (int64_t)1 << 20 && 4 * geo.n >= geo.G;
+  // (gs <= 1024: the warp engine's group tree walks gs / 32 leaves per lane
+  // serially -- a 65536-lane group would take milliseconds; LEAF splits it)
+  return c->warp_k1 && geo.G <= (int64_t)1 << 20 && 4 * geo.n >= geo.G && geo.gs <= 1024;
 }
 
 static bool mat_applies(const pk_ctx* c, const Geom& geo) {
@@ -1161,7 +1163,8 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
 #endif
   if constexpr (Op::kSpmv && NQ <= 2) {
     if constexpr (!std::decay_t<decltype(op.A)>::kSell && std::is_same<typename Op::RowT, int32_t>::value) {
-      if (c->bulk && !geo.leaf && geo.gs >= 32 && geo.K >= c->bulk_mink && geo.K <= c->bulk_maxk && NQ <= c->bulk_maxq &&
+      if (c->bulk && !geo.leaf && geo.gs >= 32 && geo.gs <= 1024 && geo.K >= c->bulk_mink && geo.K <= c->bulk_maxk &&
+          NQ <= c->bulk_maxq &&
           op.A.blk >= 0) {
         constexpr int W = PK_BULK_W, R = PK_BULK_R;
         BulkCfg bc = bulk_cfg<NQ, W, R, Op>(op.A.blk);
@@ -1200,7 +1203,7 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
   const Geom gw = k1 ? make_geom(n, c->ng, c->gs, min_units(c), true) : geo;
   if (k1 && (size_t)gw.G * (size_t)nstore > c->spill_cap)
     return fail(PK_ERR_INVALID, "engine scratch not sized (ensure_scratch)");
-  if (!gw.leaf && gw.gs >= 32 && gw.K >= (k1 ? 1 : 2) && gw.K <= 8) {
+  if (!gw.leaf && gw.gs >= 32 && gw.gs <= 1024 && gw.K >= (k1 ? 1 : 2) && gw.K <= 8) {
     const Geom& geo = gw;
     // warp-per-unit chain engine (no shared staging, no CTA barrier): wins
     // for short chains (small, latency-bound systems, e.g. CG 512^2: 20.6 vs

@@ -306,12 +306,21 @@ __device__ __forceinline__ void group_tree(const Geom& geo, int g, const double*
       for (int q = 0; q < NQ; ++q) v[q] = q < nstore ? __ldcg(spill + (int64_t)q * geo.G + base) : 0.0;
     } else {
       LeafStack<NQ> st{tail + NQ * T, T, th};
-      for (uint32_t i = 0; i < (uint32_t)geo.tm; ++i) {
-        const int64_t idx = base + (int64_t)brev_bits(i, geo.tlogm) * T;
-        double x[NQ];
+      // leaves loaded 4 at a time (one L2 round trip per batch), pushed in visit order
+      constexpr int BL = 4;
+      for (uint32_t i0 = 0; i0 < (uint32_t)geo.tm; i0 += BL) {
+        double x[BL][NQ];
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) x[q] = q < nstore ? __ldcg(spill + (int64_t)q * geo.G + idx) : 0.0;
-        st.push(i, x, v);
+        for (int b = 0; b < BL; ++b) {
+          const uint32_t i = i0 + b;
+          const int64_t idx = base + (int64_t)brev_bits(i < (uint32_t)geo.tm ? i : 0u, geo.tlogm) * T;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            x[b][q] = (q < nstore && i < (uint32_t)geo.tm) ? __ldcg(spill + (int64_t)q * geo.G + idx) : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < BL; ++b)
+          if (i0 + b < (uint32_t)geo.tm) st.push(i0 + b, x[b], v);
       }
     }
   }
