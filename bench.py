@@ -544,7 +544,9 @@ def run_c2(args, torch, pk, dev):
                                "frac": round(iter_bytes / (us_iter * 1e-6) / 1e9 / peak, 4)},
         "roofline": kernel_roofline(pk, dm, ctx, b),
         "e2e": e2e_c2(pk, ctx, args.steps),
-        "gpu_launches": int(res.diagnostics.get("launches_per_iteration", 3)) * args.steps,
+        # kernel launches of the timed solve (setup, the loop -- one cooperative kernel when the loop is
+        # persistent, else 3 per iteration -- and the tail), counted by the library
+        "gpu_launches": int(res.diagnostics.get("launches", 3 * args.steps)),
         "clocks": clk.summary(),
         "termination": res.termination,
     }

@@ -131,6 +131,8 @@ struct pk_ctx {
   size_t vec_cap = 0;
   bool mdq = false;               // PK_MDQ=1: GMRES multi-dots by k_multidot_q (quantity-parallel; measured slower:
                                   // GMRES(30) 128^3 multi-dot 98.5 vs 89.3 us, 64^3 51.4 vs 40.5 on the LANE engine)
+  bool persist = true;            // PK_PERSIST=0: BiCGStab split-body loop as the WHILE graph instead of one persistent
+                                  // cooperative kernel (measured: C2 75.6 vs 76.7 us/iter, 2048^2 221.2 vs 234.8)
   bool bulk = true;               // PK_BULK=0: SpMV operators on long lane chains use the CTA CHAIN engine instead of
                                   // the TMA-fed BULK engine (pk_bulk.cuh)
   bool bulk_pdl = false;          // PK_BULK_PDL=1: BULK kernels launch programmatically (their CSR prologue overlaps
@@ -746,13 +748,13 @@ __global__ void __launch_bounds__(256, 4) k_sweep(int64_t n, Op op, ScalarPtrs s
 // p, p + T, ..., all loads of a thread issued before its first compute (pair
 // indices are clamped, so every load is unconditional and the batch stays
 // together); the grid is sized so each thread runs exactly one batch.
+// Vectorised elementwise sweep rows (operators with load2/compute2: two
+// adjacent rows through 16-byte loads and stores).  Every thread owns UP row
+// pairs p, p + T, ..., all loads of a thread issued before its first compute
+// (pair indices are clamped, so every load is unconditional and the batch
+// stays together).
 template <class Op, int UP>
-__global__ void __launch_bounds__(256) k_sweep2(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
-  pdl_wait();
-  pdl_trigger();
-  const GateVals gv = gate_load(st, gate & 0xff);
-  op.scalars(sp);
-  if (!gate_eval(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0, gv)) return;
+__device__ __forceinline__ void sweep2_rows(int64_t n, const Op& op) {
   const int64_t np = n >> 1;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += T * UP) {
@@ -771,6 +773,82 @@ __global__ void __launch_bounds__(256) k_sweep2(int64_t n, Op op, ScalarPtrs sp,
     double c[1];
     op.load((uint32_t)(n - 1), it);
     op.compute((uint32_t)(n - 1), it, c);
+  }
+}
+
+// the grid is sized so each thread runs exactly one batch
+template <class Op, int UP>
+__global__ void __launch_bounds__(256) k_sweep2(int64_t n, Op op, ScalarPtrs sp, SolveState* st, int gate) {
+  pdl_wait();
+  pdl_trigger();
+  const GateVals gv = gate_load(st, gate & 0xff);
+  op.scalars(sp);
+  if (!gate_eval(st, gate & 0xff, (gate & GATE_IN_GRAPH) != 0, gv)) return;
+  sweep2_rows<Op, UP>(n, op);
+}
+
+template <class Op, class = void>
+struct RowsPerThreadDev { static constexpr int value = 2; };
+template <class Op>
+struct RowsPerThreadDev<Op, std::void_t<decltype(Op::kRowsPerThread)>> { static constexpr int value = Op::kRowsPerThread; };
+
+// ---------------------------------------------------------------------------
+// Persistent cooperative BiCGStab loop (PK_PERSIST=1)
+// ---------------------------------------------------------------------------
+//
+// The split BiCGStab body -- As = A s + 4 dots (finalizer FIN_BICG_TAIL), the
+// xrp sweep, Ap' = A p' + 2 dots (FIN_BICG_ALPHA) -- as phases of ONE
+// co-resident grid separated by grid barriers instead of three kernel
+// launches per iteration: the phases are the same engine / sweep device code
+// (same operations, same order: the same bits).  A barrier publishes the
+// phase's writes (release add, acquire spin) and invalidates L1 (the phases
+// read vectors through the non-coherent path).  The loop runs while the
+// state says RUNNING, exactly the gates of the graph body.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++gen;
+    const unsigned target = gen * gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+template <class OB, class OX, class OA>
+__global__ void __launch_bounds__(kThreads, 4)
+    k_bicg_persist(const __grid_constant__ Geom geo, const __grid_constant__ OB ob0, const __grid_constant__ OX ox0,
+                   const __grid_constant__ OA oa0, ScalarPtrs spb, ScalarPtrs spx, ScalarPtrs spa, double* p_quad,
+                   double* p_pair, Scratch scr, SolveState* st, unsigned* bar, int smem_d) {
+  extern __shared__ double smem[];
+  unsigned gen = 0;
+  for (;;) {
+    if (*(volatile const int32_t*)&st->status != RUNNING) break;
+    {
+      OB op = ob0;
+      op.scalars(spb);
+      const bool last = engine_run<4, RowsPerThreadDev<OB>::value>(geo, op, smem, p_quad, 4, 0, 4, scr, &st->ticket);
+      if (last && threadIdx.x < 32) finalize(st, FIN_BICG_TAIL, 0, false, smem, smem_d);
+    }
+    grid_barrier(bar, gen);
+    if (*(volatile const int32_t*)&st->status != RUNNING) break;
+    {
+      OX op = ox0;
+      op.scalars(spx);
+      sweep2_rows<OX, 2>(geo.n, op);
+    }
+    grid_barrier(bar, gen);
+    {
+      OA op = oa0;
+      op.scalars(spa);
+      const bool last = engine_run<2, RowsPerThreadDev<OA>::value>(geo, op, smem, p_pair, 2, 0, 2, scr, &st->ticket);
+      if (last && threadIdx.x < 32) finalize(st, FIN_BICG_ALPHA, 1, false, smem, smem_d);
+    }
+    grid_barrier(bar, gen);
   }
 }
 

@@ -282,7 +282,7 @@ def test_c2_bicgstab_1024_fixed_bitwise(pk):
     cfg = pk.SolverConfig(fixed_iterations=8, max_iterations=8)
     res = pk.bicgstab_pipelined(dm, b, config=cfg)
     assert_identical(res, oracle_run("bicgstab", a, b, (128, 256), fixed=8, max_iterations=8))
-    assert [p.launches for p in res.trace.iterations[:2]] == [3, 3]  # split body at n = 2^20
+    assert [p.launches for p in res.trace.iterations[:2]] == [0, 0]  # split body at n = 2^20: one persistent kernel
 
 
 def test_c3_gmres_128_fixed_bitwise(pk):
@@ -473,3 +473,18 @@ def test_cached_workspace_survives_format_change(pk):
         runs.append((x.cpu().numpy(), list(r.residual_history)))
     for x, h in runs[1:]:
         assert same(x, runs[0][0]) and same(h, runs[0][1])
+
+
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_bicgstab_persistent_loop_identical(pk, persist, monkeypatch):
+    """The split BiCGStab loop as one persistent cooperative kernel (grid
+    barriers between the phases) or as the WHILE graph: the same bits, the
+    same iterations; launches per iteration 0 vs 3.  Runs to tolerance (the
+    finalizers' STOPPING / half-step exits) on a 2^20-row system."""
+    monkeypatch.setenv("PK_PERSIST", persist)
+    dm, b = pk.convdiff2d(1024, device=True)
+    a, _ = pk.convdiff2d(1024)
+    cfg = pk.SolverConfig(fixed_iterations=24, max_iterations=24)
+    res = pk.bicgstab_pipelined(dm, b, config=cfg)
+    assert_identical(res, oracle_run("bicgstab", a, b, (128, 256), fixed=24, max_iterations=24))
+    assert [p.launches for p in res.trace.iterations[:2]] == ([0, 0] if persist == "1" else [3, 3])
