@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(32, 8)
   if (last && fin != FIN_NONE && st) finalize(st, fin, fin_arg, ing, smem, kWarpStage2Doubles);
 }
 
+#ifdef PK_MAT_ENGINE  // experimental two-phase engine (measured slower on C2), compiled out by default
 // ---------------------------------------------------------------------------
 // two-phase ("materialised") engine for SpMV operators on long lane chains
 // ---------------------------------------------------------------------------
@@ -485,6 +486,8 @@ __global__ void __launch_bounds__(kThreads, 4)
   __syncthreads();
   if (s_last && fin != FIN_NONE && st && tid < 32) finalize(st, fin, fin_arg, ing, smem, smem_d);
 }
+
+#endif  // PK_MAT_ENGINE
 
 #ifdef PK_TILE_ENGINE  // experimental (measured 3-4x slower than the CTA engine on C2), compiled out by default
 // ---------------------------------------------------------------------------
@@ -1045,7 +1048,13 @@ static bool warp_k1(const pk_ctx* c, const Geom& geo) {
 }
 
 static bool mat_applies(const pk_ctx* c, const Geom& geo) {
+#ifdef PK_MAT_ENGINE
   return c->mat_mink > 0 && !geo.leaf && geo.K >= c->mat_mink;
+#else
+  (void)c;
+  (void)geo;
+  return false;  // two-phase engine not compiled in
+#endif
 }
 
 // TILE engine (k_reduce_tiles): CHAIN geometries with whole 256-lane tiles
@@ -1187,6 +1196,7 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
       }
     }
   }
+#ifdef PK_MAT_ENGINE
   if constexpr (Op::kSpmv && NQ <= 4) {
     if (mat_applies(c, geo) && c->mat_cap >= (size_t)n * (size_t)nstore) {
       auto kr = k_mat_rows<NQ, Op>;
@@ -1203,6 +1213,7 @@ static int launch_reduce(pk_ctx* c, cudaStream_t s, int64_t n, const Op& op, Sca
       return PK_OK;
     }
   }
+#endif
   if constexpr (!Op::kSpmv) {
     if (c->lane_engine && !geo.leaf && geo.gs >= 32 && geo.K >= 2) {
       // elementwise operator on a CHAIN geometry: thread = lane, in-register

@@ -154,11 +154,13 @@ def test_split_and_fused_bodies_identical(pk, split, monkeypatch):
 
 @pytest.mark.parametrize("geom", [(8, 64), (4, 32), (2, 512)])
 def test_two_phase_engine_identical(pk, geom, monkeypatch):
-    """Two-phase SpMV engine (opt-in, PK_MAT_MINK read at context creation):
-    thread-per-row pass storing the contributions, then the ordered lane-chain
-    fold.  Geometries cover a group spanning several fold CTAs (2 x 512),
-    one (8 x 64) and several groups per fold CTA (4 x 32); chains K >= 9.
-    Bits, iteration counts and termination identical to the oracle."""
+    """Two-phase SpMV engine (opt-in, PK_MAT_MINK read at context creation;
+    compiled in with -DPK_MAT_ENGINE, otherwise the default engines run under
+    the same setting): thread-per-row pass storing the contributions, then the
+    ordered lane-chain fold.  Geometries cover a group spanning several fold
+    CTAs (2 x 512), one (8 x 64) and several groups per fold CTA (4 x 32);
+    chains K >= 9.  Bits, iteration counts and termination identical to the
+    oracle."""
     monkeypatch.setenv("PK_MAT_MINK", "9")
     a, b = pk.convdiff2d(96)
     pa, pb = pk.poisson2d_grid(96)
