@@ -13,15 +13,18 @@ funcs = re.split(r"\n\s*Function : ", text)
 want = {"OpBicgB<int, 5, false>": "k_reduce_OpBicgB", "OpBicgApNext<int, 5, false>": "k_reduce_OpBicgApNext",
         "k_sweep2<pk::OpBicgXrpSweep, 4>": "k_sweep2_OpBicgXrpSweep", "k_sweep2<pk::OpCgXSweep, 4>": "k_sweep2_OpCgXSweep",
         "OpCgFused<int, 5, false>": "k_reduce_warp_OpCgFused", "k_spmv_ell": "k_spmv_ell",
-        "k_vec_update<1>": "k_vec_update_axpy2"}
+        "k_vec_update<1>": "k_vec_update_axpy2",
+        "k_reduce_bulk<2, 4, 3, 7, pk::OpBicgApNext<int, 5, false> >": "k_reduce_bulk_OpBicgApNext",
+        "k_rowsum_warp<pk::OpCgFused<int, 7, false> >": "k_rowsum_warp_OpCgFused",
+        "k_bicg_persist<pk::OpBicgB<int, 5, false>": "k_bicg_persist"}
 rows = []
 for f in funcs[1:]:
     name = f.split("\n", 1)[0].strip()
     dem = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip()
     for key, tag in want.items():
         if key in dem and (("k_reduce<" in dem and "warp" not in tag) or ("k_reduce_warp<" in dem and "warp" in tag)
-                           or ("k_reduce" not in dem)):
-            if "k_reduce" in tag and "<4, 2, 4," not in dem and "<2, 2, 4," not in dem and "warp" not in tag:
+                           or ("k_reduce" not in dem) or dem.split("(")[0].startswith("void " + key.split("<")[0]) and "<" in key):
+            if tag.startswith("k_reduce_Op") and "<4, 2, 4," not in dem and "<2, 2, 4," not in dem:
                 continue
             open(f"{out}/{tag}.sass", "w").write(dem + "\n" + f)
             ins = re.findall(r"/\*[0-9a-f]{4,}\*/\s+(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]+)", f)
@@ -29,16 +32,19 @@ for f in funcs[1:]:
             cnt = lambda p: sum(1 for o in ops if o.startswith(p))
             rows.append((tag, len(ops), cnt("LDG"), sum(1 for o in ops if o.startswith("LDG") and ".128" in o),
                          cnt("STG"), sum(1 for o in ops if o.startswith("STG") and ".128" in o), cnt("LDS"),
-                         cnt("DADD"), cnt("DMUL"), cnt("DFMA"), cnt("BAR"), cnt("ATOM") + cnt("RED")))
+                         cnt("DADD"), cnt("DMUL"), cnt("DFMA"), cnt("BAR"), cnt("ATOM") + cnt("RED"),
+                         cnt("UBLKCP"), cnt("SYNCS")))
             want.pop(key)
             break
 with open(f"{out}/README.md", "w") as fh:
     fh.write("# SASS of the hot kernels (sm_100a, cuobjdump -sass of libpk_b200.so)\n\n"
              "Static instruction counts. DFMA appears only inside the correctly rounded div.rn / sqrt.rn\n"
              "expansions of the finalizers (the row arithmetic is DMUL + DADD, -fmad=false).\n\n"
-             "LDG.128 / STG.128 = 16-byte vector accesses (the k_sweep2 streaming kernels).\n\n"
-             "| kernel | instructions | LDG | LDG.128 | STG | STG.128 | LDS | DADD | DMUL | DFMA | BAR | ATOM/RED |\n"
-             "|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+             "LDG.128 / STG.128 = 16-byte vector accesses (the k_sweep2 streaming kernels).  UBLKCP = cp.async.bulk\n"
+             "(TMA 1-D bulk copy, the BULK engine's CSR feed); SYNCS = mbarrier operations (arrive / expect_tx /\n"
+             "try_wait).  k_bicg_persist = the persistent cooperative BiCGStab loop (three phases + grid barriers).\n\n"
+             "| kernel | instructions | LDG | LDG.128 | STG | STG.128 | LDS | DADD | DMUL | DFMA | BAR | ATOM/RED | UBLKCP | SYNCS |\n"
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
     for r in rows:
         fh.write("| " + " | ".join(str(v) for v in r) + " |\n")
 print(open(f"{out}/README.md").read())
