@@ -163,8 +163,14 @@ def test_c2_1024_to_tolerance_bitwise(pk):
     assert_bitwise(res, "c2_1024_tol")
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
 @pytest.mark.parametrize("name", ["bicgstab_check_pass", "bicgstab_check_resume", "bicgstab_check_resume_g1x4"])
-def test_bicgstab_check_phase_bitwise(pk, name):
+def test_bicgstab_check_phase_bitwise(pk, name, split, monkeypatch):
+    """The clamped-identity "check" phase (solvers.py:687-694), passing and
+    failing-then-resuming; split = 1 forces the split body, which on these
+    CHAIN geometries runs as the persistent cooperative loop -- relaunched
+    after every failed check."""
+    monkeypatch.setenv("PK_BICG_SPLIT", split)
     meta, store = case(name)
     spec = json.loads((GOLD / "scale_check_spec.json").read_text())[name]
     a = pk.CsrMatrix.from_dense(spec["dense"])
