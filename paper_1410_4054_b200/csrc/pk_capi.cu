@@ -807,6 +807,9 @@ struct RowsPerThreadDev<Op, std::void_t<decltype(Op::kRowsPerThread)>> { static 
 // phase's writes (release add, acquire spin) and invalidates L1 (the phases
 // read vectors through the non-coherent path).  The loop runs while the
 // state says RUNNING, exactly the gates of the graph body.
+#ifndef PK_BAR_SLEEP_NS
+#define PK_BAR_SLEEP_NS 32
+#endif
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -814,9 +817,13 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
     const unsigned target = gen * gridDim.x;
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     unsigned v;
-    do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    while (v < target) {
+      // back off: ~600 CTAs polling one L2 line would compete with the
+      // phase's last CTAs (group trees, finalizer) for that L2 slice
+      __nanosleep(PK_BAR_SLEEP_NS);
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
+    }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
