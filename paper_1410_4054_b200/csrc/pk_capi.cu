@@ -871,6 +871,27 @@ __global__ void k_spin(long long cycles) {
   }
 }
 
+// Persistent cooperative CG loop (fused body on the pipelined lane engine,
+// short lane chains -- C1): one phase per iteration (OpCgFused + FIN_CG_FUSED)
+// and a grid barrier instead of one WHILE-graph kernel node per iteration.
+// The lane engine maps lanes to CTAs one to one (grid = G / T, co-resident at
+// one CTA per SM); same device code, same bits.
+template <class Op>
+__global__ void __launch_bounds__(kLaneThreads, 1)
+    k_cg_persist(const __grid_constant__ Geom geo, const __grid_constant__ Op op0, ScalarPtrs sp, double* part,
+                 Scratch scr, SolveState* st, unsigned* bar, int smem_d) {
+  extern __shared__ double smem[];
+  unsigned gen = 0;
+  for (;;) {
+    if (*(volatile const int32_t*)&st->status != RUNNING) break;
+    Op op = op0;
+    op.scalars(sp);
+    const bool last = engine_lane_spmv<3, PK_LANE_P>(geo, op, smem, part, 3, 0, 3, scr, &st->ticket);
+    if (last && threadIdx.x < 32) finalize(st, FIN_CG_FUSED, 0, false, smem, smem_d);
+    grid_barrier(bar, gen);
+  }
+}
+
 __global__ void k_finalize(SolveState* st, int fin, int arg) {
   __shared__ double buf[1024];
   finalize(st, fin, arg, false, buf, 1024);
